@@ -1,0 +1,199 @@
+/*
+ * lutgemm.h -- C ABI of the B200-native LUT-GEMM hot path (arXiv 2206.09557).
+ *
+ * The operation (Sec. 3.2, with the Eq. 3 bias):
+ *
+ *     y[beta][r] = sum_c ( sum_{i<q} alpha[r][c/g][i] * b_i[r][c] + z[r][c/g] ) * x[beta][c]
+ *
+ * for a q-bit extended-BCQ weight W (m rows, n reduction columns), binary
+ * planes b_i in {-1,+1}, group-wise scales alpha shared by g consecutive columns
+ * (Sec. 3.4), optional bias z (Eq. 3), and fp16 activations.  The
+ * kernels evaluate it as the paper does: one lookup table of all 2^8 signed
+ * partial sums per 8-column chunk of x, built in shared memory (mu = 8,
+ * P:L192-199, App. B), indexed by the packed sign bits.
+ *
+ * Conventions (all calls):
+ *  - Plain C.  fp16 values travel as uint16_t bit patterns (IEEE binary16).
+ *  - "device" pointers are CUDA global-memory pointers on the current device;
+ *    "host" pointers are CPU memory.  The library never allocates on the hot
+ *    path; every buffer is caller-owned (the Python binding uses PyTorch
+ *    tensors for this).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Every device call is asynchronous on that stream; launch errors return
+ *    LUTGEMM_ERR_CUDA, execution errors surface at stream synchronisation.
+ *  - No C++ exception crosses the ABI.  On any non-OK status,
+ *    lutgemm_last_error() returns a thread-local description.
+ *  - The library is stateless except for an explicit TP communicator and the
+ *    thread-local error text; calls on distinct outputs/workspaces are
+ *    thread-safe.
+ *  - Supported shapes on the GPU path: n % 32 == 0, g % 32 == 0, n % g == 0
+ *    (g == n is row-wise, P:L496 '-' / P:L392 "g=m"), 1 <= q <= 8, m >= 1,
+ *    1 <= b <= 32.  Anything else returns LUTGEMM_ERR_INVALID_ARG (DESIGN.md
+ *    reading R13: the paper does not define chunks straddling a group).
+ *  - Requires an sm_100 device (B200); otherwise LUTGEMM_ERR_UNSUPPORTED.
+ */
+#ifndef LUTGEMM_H_
+#define LUTGEMM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LUTGEMM_ABI_VERSION 1
+
+typedef enum {
+  LUTGEMM_OK = 0,
+  LUTGEMM_ERR_INVALID_ARG = 1, /* shape rule above violated, NULL pointer, bad enum */
+  LUTGEMM_ERR_MISALIGNED = 2,  /* a device pointer violates the stated alignment */
+  LUTGEMM_ERR_WORKSPACE = 3,   /* ws too small (see lutgemm_workspace_bytes) */
+  LUTGEMM_ERR_CUDA = 4,        /* CUDA runtime error (launch / attribute / device) */
+  LUTGEMM_ERR_NCCL = 5,        /* NCCL error in a lutgemm_tp_* call */
+  LUTGEMM_ERR_UNSUPPORTED = 6  /* current device is not sm_100 */
+} lutgemm_status;
+
+/* A packed weight in the kernel-native layout (opaque byte order; see
+ * DESIGN.md "Data layout in HBM").  The struct itself lives on the host; the
+ * three buffers live on the device and are owned by the caller.
+ *   planes : lutgemm_packed_bytes().planes bytes, 16-byte aligned
+ *   alpha  : lutgemm_packed_bytes().alpha bytes, 16-byte aligned (fp16)
+ *   offset : lutgemm_packed_bytes().offset bytes, 16-byte aligned (fp16), or
+ *            NULL when has_offset == 0 (z = 0). */
+typedef struct {
+  int32_t m, n, q, g;
+  int32_t has_offset;
+  int32_t reserved;
+  void* planes;
+  void* alpha;
+  void* offset;
+} lutgemm_weight;
+
+enum { LUTGEMM_SRC_BCQ = 0, LUTGEMM_SRC_UNIFORM = 1 };
+
+/* Source of a pack call, canonical layout, all device pointers.
+ * BCQ (non-uniform, Eq. 3):
+ *   planes : uint32 [q][m][n/32]; bit j of word w of row r of plane i is
+ *            b_i[r][32w+j]; bit 1 means +1, bit 0 means -1 (R1, from
+ *            b = 2*b_hat - 1).  Plane 0 first (R4).
+ *   alpha  : fp16 [m][n/g][q]      (scale per row, group, plane; R7)
+ *   offset : fp16 [m][n/g] or NULL (bias z per row and group; R5)
+ * UNIFORM (App. C): w = s * code + z_hat (Eq. 6), converted on the
+ * device to alpha_i = 2^(i-1) s, b_i = 2 * bit_i(code) - 1,
+ * z = sum_i alpha_i + z_hat (Eq. 8), stored as fp16 (round to nearest even;
+ * z is summed in fp64 before the single rounding, R17).
+ *   codes  : uint8 [m][n], 0 <= code < 2^q
+ *   scale  : fp16 [m][n/g]  (s)
+ *   zero   : fp16 [m][n/g]  (z_hat, additive; an integer zero-point zp maps to
+ *            z_hat = -s * zp, R16)
+ * Source pointers need only their natural element alignment. */
+typedef struct {
+  int32_t kind; /* LUTGEMM_SRC_BCQ | LUTGEMM_SRC_UNIFORM */
+  int32_t m, n, q, g;
+  int32_t reserved;
+  const uint32_t* planes;
+  const uint16_t* alpha;
+  const uint16_t* offset;
+  const uint8_t* codes;
+  const uint16_t* scale;
+  const uint16_t* zero;
+} lutgemm_pack_src;
+
+/* Library ABI version (LUTGEMM_ABI_VERSION). */
+int lutgemm_abi_version(void);
+
+/* Thread-local text for the last non-OK status returned on this thread. */
+const char* lutgemm_last_error(void);
+
+/* Byte sizes of the three native buffers for an (m, n, q, g) weight.
+ * offset_bytes is 0 when has_offset == 0.  Pure host computation. */
+lutgemm_status lutgemm_packed_bytes(int m, int n, int q, int g, int has_offset,
+                                    size_t* planes_bytes, size_t* alpha_bytes,
+                                    size_t* offset_bytes);
+
+/* Repack a canonical BCQ or uniform source into dst's native buffers (which
+ * the caller allocated with lutgemm_packed_bytes sizes and set in dst).  The
+ * call fills dst->m, n, q, g, has_offset (has_offset = 1 for UNIFORM, and for
+ * BCQ iff src->offset != NULL).  Offline step (App. C "two-step methodology",
+ * P:L615-620); asynchronous on `stream`. */
+lutgemm_status lutgemm_pack_bcq(const lutgemm_pack_src* src, lutgemm_weight* dst, void* stream);
+
+/* Inverse of the BCQ pack (test-only): native -> canonical planes / alpha /
+ * offset (offset may be NULL).  Bit-exact round trip. */
+lutgemm_status lutgemm_unpack_bcq(const lutgemm_weight* w, uint32_t* planes, uint16_t* alpha,
+                                  uint16_t* offset, void* stream);
+
+/* Workspace for a product with m rows, n columns, batch b: fp32 split-K
+ * partials plus row-block arrival counters.  The workspace must be zeroed
+ * once (lutgemm_workspace_init) before its first use; every successful call
+ * leaves it ready for the next.  One workspace must not be used by two calls
+ * that may run concurrently. */
+size_t lutgemm_workspace_bytes(int m, int n, int b);
+lutgemm_status lutgemm_workspace_init(void* ws, size_t ws_bytes, void* stream);
+
+/* y = W x for one fp16 activation vector (b = 1), the paper's single-batch
+ * case.  x: device fp16 [n], 16-byte aligned.  y: device fp16 [m],
+ * 2-byte aligned, rounded to nearest even from an fp32 accumulation (R12).
+ * ws: device, 16-byte aligned, >= lutgemm_workspace_bytes(m, n, 1).
+ * Deterministic: fixed-order reductions, bitwise reproducible (R11). */
+lutgemm_status lutgemm_gemv(const lutgemm_weight* w, const uint16_t* x, uint16_t* y, void* ws,
+                            size_t ws_bytes, void* stream);
+
+/* Y = X W^T for b activation rows (1 <= b <= 32): X device fp16 [b][n]
+ * (16-byte aligned, rows contiguous), Y device fp16 [b][m].  Same LUT method,
+ * one table bank per activation row sharing each key. */
+lutgemm_status lutgemm_gemm_batched(const lutgemm_weight* w, const uint16_t* X, int b, uint16_t* Y,
+                                    void* ws, size_t ws_bytes, void* stream);
+
+/* As lutgemm_gemm_batched but writes the fp32 result Yf [b][m] (no fp16
+ * rounding): the local partial of a column-split tensor-parallel shard. */
+lutgemm_status lutgemm_gemm_batched_f32(const lutgemm_weight* w, const uint16_t* X, int b, float* Yf,
+                                        void* ws, size_t ws_bytes, void* stream);
+
+/* End-to-end call with HOST activations and outputs: copies X_host [b][n]
+ * (fp16, ideally pinned) to the device staging area inside ws, runs the
+ * product, copies Y [b][m] back to Y_host and synchronises `stream` before
+ * returning.  ws (device, 16-byte aligned) must hold
+ * lutgemm_host_workspace_bytes(m, n, b) bytes and be initialised like any
+ * workspace.  The weight stays resident on the device. */
+size_t lutgemm_host_workspace_bytes(int m, int n, int b);
+lutgemm_status lutgemm_gemm_host(const lutgemm_weight* w, const uint16_t* X_host, int b, uint16_t* Y_host,
+                                 void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------- Tensor parallelism over NCCL (NVLink / NVSwitch) ----------------
+ * The paper runs LUT-GEMM tensor-parallel on 1/2/4/8 GPUs (P:L378-385,
+ * Table 2, Tables 3/4) and names communication as what limits it
+ * (P:L411-413).  One process per GPU; the NCCL unique id is produced on rank
+ * 0 and broadcast by the caller (the Python binding uses torch.distributed). */
+typedef struct lutgemm_tp lutgemm_tp;
+
+enum {
+  LUTGEMM_TP_ROWS_LOCAL = 0,     /* shard = rows [r*m/P,(r+1)*m/P); x full; y = local rows only */
+  LUTGEMM_TP_ROWS_ALLGATHER = 1, /* same shard; y = full [b][m] replicated via ncclAllGather */
+  LUTGEMM_TP_COLS_ALLREDUCE = 2  /* shard = columns [r*n/P,(r+1)*n/P) (multiple of g); x = local
+                                    slice [b][n/P]; fp32 partials ncclAllReduce(sum), then fp16 y [b][m] */
+};
+
+/* 128-byte opaque NCCL unique id, to be created on rank 0 only. */
+lutgemm_status lutgemm_tp_unique_id(uint8_t id[128]);
+/* Create the communicator (collective over all ranks; current CUDA device is used). */
+lutgemm_status lutgemm_tp_init(int nranks, int rank, const uint8_t id[128], lutgemm_tp** out);
+/* Workspace for lutgemm_tp_linear with this shard and mode. */
+size_t lutgemm_tp_workspace_bytes(const lutgemm_tp* tp, int mode, int m_shard, int n_shard, int b);
+/* One tensor-parallel linear: the shard's LUT-GEMM followed by the mode's
+ * collective, all on `stream` (graph-capturable).  `shard` is this rank's
+ * packed shard (m_shard x n_shard).  y layout per mode as above; for
+ * ROWS_ALLGATHER y is [b][P*m_shard].  ws is >= lutgemm_tp_workspace_bytes. */
+lutgemm_status lutgemm_tp_linear(lutgemm_tp* tp, int mode, const lutgemm_weight* shard,
+                                 const uint16_t* x, int b, uint16_t* y, void* ws, size_t ws_bytes,
+                                 void* stream);
+lutgemm_status lutgemm_tp_destroy(lutgemm_tp* tp);
+int lutgemm_tp_rank(const lutgemm_tp* tp);
+int lutgemm_tp_nranks(const lutgemm_tp* tp);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LUTGEMM_H_ */

@@ -1,0 +1,234 @@
+// lutgemm_abi.cu -- the extern "C" boundary declared in include/lutgemm.h:
+// argument validation, status codes, thread-local error text, dispatch.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "layout.cuh"
+#include "lutgemm.h"
+#include "lutgemm_internal.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+lutgemm_status fail(lutgemm_status st, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return st;
+}
+
+lutgemm_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(LUTGEMM_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+lutgemm_status check_shape(int m, int n, int q, int g) {
+  if (m < 1) return fail(LUTGEMM_ERR_INVALID_ARG, "m=%d must be >= 1", m);
+  if (n < 32 || n % 32) return fail(LUTGEMM_ERR_INVALID_ARG, "n=%d must be a positive multiple of 32", n);
+  if (q < 1 || q > 8) return fail(LUTGEMM_ERR_INVALID_ARG, "q=%d must be in [1, 8]", q);
+  if (g < 32 || g % 32 || n % g)
+    return fail(LUTGEMM_ERR_INVALID_ARG, "g=%d must be a multiple of 32 dividing n=%d (g=n is row-wise)", g, n);
+  if ((long long)m * (n / 32) >= (1LL << 40)) return fail(LUTGEMM_ERR_INVALID_ARG, "shape too large");
+  return LUTGEMM_OK;
+}
+
+int g_dev_ok[64];  // 0 unknown, 1 ok, 2 unsupported
+
+lutgemm_status check_device() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!g_dev_ok[dev]) {
+    int major = 0, minor = 0;
+    e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    g_dev_ok[dev] = (major == 10 && minor == 0) ? 1 : 2;
+    if (g_dev_ok[dev] == 2)
+      return fail(LUTGEMM_ERR_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a only", dev, major,
+                  minor);
+  }
+  if (g_dev_ok[dev] == 2) return fail(LUTGEMM_ERR_UNSUPPORTED, "device %d is not sm_100", dev);
+  return LUTGEMM_OK;
+}
+
+lutgemm_status check_weight(const lutgemm_weight* w) {
+  if (!w) return fail(LUTGEMM_ERR_INVALID_ARG, "weight is NULL");
+  lutgemm_status st = check_shape(w->m, w->n, w->q, w->g);
+  if (st != LUTGEMM_OK) return st;
+  if (!w->planes || !w->alpha) return fail(LUTGEMM_ERR_INVALID_ARG, "weight planes/alpha is NULL");
+  if (w->has_offset && !w->offset) return fail(LUTGEMM_ERR_INVALID_ARG, "has_offset=1 but offset is NULL");
+  if (!aligned(w->planes, 16) || !aligned(w->alpha, 16) || (w->has_offset && !aligned(w->offset, 16)))
+    return fail(LUTGEMM_ERR_MISALIGNED, "weight buffers must be 16-byte aligned");
+  return LUTGEMM_OK;
+}
+
+lutgemm_status product(const lutgemm_weight* w, const uint16_t* X, int b, uint16_t* Y, float* Yf, void* ws,
+                       size_t ws_bytes, void* stream) {
+  lutgemm_status st = check_weight(w);
+  if (st != LUTGEMM_OK) return st;
+  if (b < 1 || b > 32) return fail(LUTGEMM_ERR_INVALID_ARG, "b=%d must be in [1, 32]", b);
+  if (!X || (!Y && !Yf) || !ws) return fail(LUTGEMM_ERR_INVALID_ARG, "x, y and ws must be non-NULL");
+  if (!aligned(X, 16)) return fail(LUTGEMM_ERR_MISALIGNED, "x must be 16-byte aligned");
+  if (!aligned(ws, 16)) return fail(LUTGEMM_ERR_MISALIGNED, "ws must be 16-byte aligned");
+  if (Y && !aligned(Y, 2)) return fail(LUTGEMM_ERR_MISALIGNED, "y must be 2-byte aligned");
+  if (Yf && !aligned(Yf, 4)) return fail(LUTGEMM_ERR_MISALIGNED, "yf must be 4-byte aligned");
+  const lg::Shape sh = lg::make_shape(w->m, w->n, w->q, w->g);
+  const size_t need = lg::workspace_bytes(sh, b);
+  if (ws_bytes < need) return fail(LUTGEMM_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, need);
+  st = check_device();
+  if (st != LUTGEMM_OK) return st;
+  cudaError_t e = lg::run_product(sh, w->planes, w->alpha, w->has_offset ? w->offset : nullptr, X, b, Y, Yf, ws,
+                                  static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "LUT-GEMM kernel launch");
+  return LUTGEMM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lutgemm_abi_version(void) { return LUTGEMM_ABI_VERSION; }
+
+const char* lutgemm_last_error(void) { return g_err; }
+
+lutgemm_status lutgemm_packed_bytes(int m, int n, int q, int g, int has_offset, size_t* planes_bytes,
+                                    size_t* alpha_bytes, size_t* offset_bytes) {
+  lutgemm_status st = check_shape(m, n, q, g);
+  if (st != LUTGEMM_OK) return st;
+  const lg::Shape sh = lg::make_shape(m, n, q, g);
+  if (planes_bytes) *planes_bytes = lg::planes_bytes(sh);
+  if (alpha_bytes) *alpha_bytes = lg::alpha_elems(sh) * 2u;
+  if (offset_bytes) *offset_bytes = has_offset ? lg::offset_elems(sh) * 2u : 0u;
+  return LUTGEMM_OK;
+}
+
+lutgemm_status lutgemm_pack_bcq(const lutgemm_pack_src* src, lutgemm_weight* dst, void* stream) {
+  if (!src || !dst) return fail(LUTGEMM_ERR_INVALID_ARG, "src/dst is NULL");
+  lutgemm_status st = check_shape(src->m, src->n, src->q, src->g);
+  if (st != LUTGEMM_OK) return st;
+  const bool uniform = src->kind == LUTGEMM_SRC_UNIFORM;
+  if (src->kind != LUTGEMM_SRC_BCQ && !uniform) return fail(LUTGEMM_ERR_INVALID_ARG, "bad src kind %d", src->kind);
+  if (uniform) {
+    if (!src->codes || !src->scale || !src->zero)
+      return fail(LUTGEMM_ERR_INVALID_ARG, "uniform source needs codes, scale and zero");
+  } else if (!src->planes || !src->alpha) {
+    return fail(LUTGEMM_ERR_INVALID_ARG, "BCQ source needs planes and alpha");
+  }
+  const int has_offset = uniform ? 1 : (src->offset != nullptr);
+  if (!dst->planes || !dst->alpha || (has_offset && !dst->offset))
+    return fail(LUTGEMM_ERR_INVALID_ARG, "destination buffers not set");
+  if (!aligned(dst->planes, 16) || !aligned(dst->alpha, 16) || (has_offset && !aligned(dst->offset, 16)))
+    return fail(LUTGEMM_ERR_MISALIGNED, "destination buffers must be 16-byte aligned");
+  if ((src->planes && !aligned(src->planes, 4)) || (src->alpha && !aligned(src->alpha, 2)) ||
+      (src->offset && !aligned(src->offset, 2)) || (src->scale && !aligned(src->scale, 2)) ||
+      (src->zero && !aligned(src->zero, 2)))
+    return fail(LUTGEMM_ERR_MISALIGNED, "source buffers must be element-aligned");
+  st = check_device();
+  if (st != LUTGEMM_OK) return st;
+  const lg::Shape sh = lg::make_shape(src->m, src->n, src->q, src->g);
+  cudaError_t e;
+  if (uniform)
+    e = lg::run_pack_uniform(sh, src->codes, src->scale, src->zero, dst->planes, dst->alpha, dst->offset,
+                             static_cast<cudaStream_t>(stream));
+  else
+    e = lg::run_pack_bcq(sh, src->planes, src->alpha, src->offset, dst->planes, dst->alpha, dst->offset,
+                         static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "pack kernel launch");
+  dst->m = src->m;
+  dst->n = src->n;
+  dst->q = src->q;
+  dst->g = src->g;
+  dst->has_offset = has_offset;
+  dst->reserved = 0;
+  if (!has_offset) dst->offset = nullptr;
+  return LUTGEMM_OK;
+}
+
+lutgemm_status lutgemm_unpack_bcq(const lutgemm_weight* w, uint32_t* planes, uint16_t* alpha, uint16_t* offset,
+                                  void* stream) {
+  lutgemm_status st = check_weight(w);
+  if (st != LUTGEMM_OK) return st;
+  if (offset && !w->has_offset) return fail(LUTGEMM_ERR_INVALID_ARG, "weight has no offset to unpack");
+  st = check_device();
+  if (st != LUTGEMM_OK) return st;
+  const lg::Shape sh = lg::make_shape(w->m, w->n, w->q, w->g);
+  cudaError_t e = lg::run_unpack(sh, w->planes, w->alpha, w->has_offset ? w->offset : nullptr, planes, alpha,
+                                 offset, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "unpack kernel launch");
+  return LUTGEMM_OK;
+}
+
+size_t lutgemm_workspace_bytes(int m, int n, int b) {
+  if (m < 1 || n < 32 || b < 1) return 0;
+  const lg::Shape sh = lg::make_shape(m, n, 1, n);
+  return lg::workspace_bytes(sh, b);
+}
+
+lutgemm_status lutgemm_workspace_init(void* ws, size_t ws_bytes, void* stream) {
+  if (!ws) return fail(LUTGEMM_ERR_INVALID_ARG, "ws is NULL");
+  cudaError_t e = cudaMemsetAsync(ws, 0, ws_bytes, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(ws)");
+  return LUTGEMM_OK;
+}
+
+lutgemm_status lutgemm_gemv(const lutgemm_weight* w, const uint16_t* x, uint16_t* y, void* ws, size_t ws_bytes,
+                            void* stream) {
+  if (!y) return fail(LUTGEMM_ERR_INVALID_ARG, "y is NULL");
+  return product(w, x, 1, y, nullptr, ws, ws_bytes, stream);
+}
+
+lutgemm_status lutgemm_gemm_batched(const lutgemm_weight* w, const uint16_t* X, int b, uint16_t* Y, void* ws,
+                                    size_t ws_bytes, void* stream) {
+  if (!Y) return fail(LUTGEMM_ERR_INVALID_ARG, "Y is NULL");
+  return product(w, X, b, Y, nullptr, ws, ws_bytes, stream);
+}
+
+lutgemm_status lutgemm_gemm_batched_f32(const lutgemm_weight* w, const uint16_t* X, int b, float* Yf, void* ws,
+                                        size_t ws_bytes, void* stream) {
+  if (!Yf) return fail(LUTGEMM_ERR_INVALID_ARG, "Yf is NULL");
+  return product(w, X, b, nullptr, Yf, ws, ws_bytes, stream);
+}
+
+static size_t align256(size_t v) { return (v + 255) / 256 * 256; }
+
+size_t lutgemm_host_workspace_bytes(int m, int n, int b) {
+  const size_t base = lutgemm_workspace_bytes(m, n, b);
+  if (!base) return 0;
+  return align256(base) + align256((size_t)b * n * 2) + align256((size_t)b * m * 2);
+}
+
+lutgemm_status lutgemm_gemm_host(const lutgemm_weight* w, const uint16_t* X_host, int b, uint16_t* Y_host, void* ws,
+                                 size_t ws_bytes, void* stream) {
+  lutgemm_status st = check_weight(w);
+  if (st != LUTGEMM_OK) return st;
+  if (!X_host || !Y_host || !ws) return fail(LUTGEMM_ERR_INVALID_ARG, "X_host, Y_host and ws must be non-NULL");
+  if (b < 1 || b > 32) return fail(LUTGEMM_ERR_INVALID_ARG, "b=%d must be in [1, 32]", b);
+  const size_t need = lutgemm_host_workspace_bytes(w->m, w->n, b);
+  if (ws_bytes < need) return fail(LUTGEMM_ERR_WORKSPACE, "host workspace %zu bytes < required %zu", ws_bytes, need);
+  const size_t pws = align256(lutgemm_workspace_bytes(w->m, w->n, b));
+  uint8_t* xd = static_cast<uint8_t*>(ws) + pws;
+  uint8_t* yd = xd + align256((size_t)b * w->n * 2);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemcpyAsync(xd, X_host, (size_t)b * w->n * 2, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync H2D");
+  st = product(w, reinterpret_cast<uint16_t*>(xd), b, reinterpret_cast<uint16_t*>(yd), nullptr, ws, pws, stream);
+  if (st != LUTGEMM_OK) return st;
+  e = cudaMemcpyAsync(Y_host, yd, (size_t)b * w->m * 2, cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync D2H");
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+  return LUTGEMM_OK;
+}
+
+}  // extern "C"
+
+// exported for the TP translation unit
+lutgemm_status lutgemm_internal_fail(lutgemm_status st, const char* msg) { return fail(st, "%s", msg); }

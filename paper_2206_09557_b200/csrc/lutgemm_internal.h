@@ -1,0 +1,47 @@
+// lutgemm_internal.h -- declarations shared by the kernel and ABI translation units.
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "layout.cuh"
+
+namespace lg {
+
+struct KParams {
+  const uint8_t* planes;
+  const __half* alpha;
+  const __half* offset;
+  const __half* x;   // [b][n]
+  __half* y;         // [b][m] fp16 output (or null)
+  float* yf;         // [b][m] fp32 output (or null)
+  float* partial;    // [S][b][m4] split-K partials
+  unsigned* counters;
+  Shape sh;
+  int b;
+  int bl;            // log2 of the table-bank count B >= b
+  long long items;
+};
+
+size_t counters_bytes(const Shape& sh);
+size_t workspace_bytes(const Shape& sh, int b);
+
+// y (fp16) or yf (fp32) [b][m] = X [b][n] W^T.  One kernel launch.
+cudaError_t run_product(const Shape& sh, const void* planes, const void* alpha, const void* offset,
+                        const uint16_t* x, int b, uint16_t* y, float* yf, void* ws, cudaStream_t st);
+
+cudaError_t run_pack_bcq(const Shape& sh, const uint32_t* planes, const uint16_t* alpha, const uint16_t* offset,
+                         void* dplanes, void* dalpha, void* doffset, cudaStream_t st);
+cudaError_t run_pack_uniform(const Shape& sh, const uint8_t* codes, const uint16_t* scale, const uint16_t* zero,
+                             void* dplanes, void* dalpha, void* doffset, cudaStream_t st);
+cudaError_t run_unpack(const Shape& sh, const void* dplanes, const void* dalpha, const void* doffset,
+                       uint32_t* planes, uint16_t* alpha, uint16_t* offset, cudaStream_t st);
+
+// TP helpers
+cudaError_t run_cast_f32_f16(const float* src, uint16_t* dst, size_t count, cudaStream_t st);
+// src [P][b][ms] -> dst [b][P*ms]
+cudaError_t run_gather_permute(const uint16_t* src, uint16_t* dst, int P, int b, int ms, cudaStream_t st);
+
+}  // namespace lg

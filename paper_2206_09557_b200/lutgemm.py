@@ -1,0 +1,262 @@
+"""ctypes binding of liblutgemm.so (include/lutgemm.h) -- argument marshalling only.
+
+Every step of the LUT-GEMM path runs in the CUDA library; this module only
+turns PyTorch tensors (device memory, streams) into pointers and sizes.  There
+is no CPU fallback: importing this module without the built library raises.
+Function names mirror the C ABI.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblutgemm.so")
+
+OK = 0
+STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "MISALIGNED", 3: "WORKSPACE", 4: "CUDA", 5: "NCCL", 6: "UNSUPPORTED"}
+SRC_BCQ, SRC_UNIFORM = 0, 1
+TP_ROWS_LOCAL, TP_ROWS_ALLGATHER, TP_COLS_ALLREDUCE = 0, 1, 2
+
+
+class LutgemmError(RuntimeError):
+    def __init__(self, fn: str, status: int, msg: str):
+        super().__init__(f"{fn} -> {STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class lutgemm_weight(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int32), ("n", ctypes.c_int32), ("q", ctypes.c_int32), ("g", ctypes.c_int32),
+                ("has_offset", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("planes", ctypes.c_void_p), ("alpha", ctypes.c_void_p), ("offset", ctypes.c_void_p)]
+
+
+class lutgemm_pack_src(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("m", ctypes.c_int32), ("n", ctypes.c_int32), ("q", ctypes.c_int32),
+                ("g", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("planes", ctypes.c_void_p), ("alpha", ctypes.c_void_p), ("offset", ctypes.c_void_p),
+                ("codes", ctypes.c_void_p), ("scale", ctypes.c_void_p), ("zero", ctypes.c_void_p)]
+
+
+# (name, restype, argtypes) of every symbol include/lutgemm.h declares
+_P = ctypes.c_void_p
+_SZ = ctypes.c_size_t
+_I = ctypes.c_int
+SIGNATURES = [
+    ("lutgemm_abi_version", _I, []),
+    ("lutgemm_last_error", ctypes.c_char_p, []),
+    ("lutgemm_packed_bytes", _I, [_I, _I, _I, _I, _I, ctypes.POINTER(_SZ), ctypes.POINTER(_SZ), ctypes.POINTER(_SZ)]),
+    ("lutgemm_pack_bcq", _I, [ctypes.POINTER(lutgemm_pack_src), ctypes.POINTER(lutgemm_weight), _P]),
+    ("lutgemm_unpack_bcq", _I, [ctypes.POINTER(lutgemm_weight), _P, _P, _P, _P]),
+    ("lutgemm_workspace_bytes", _SZ, [_I, _I, _I]),
+    ("lutgemm_workspace_init", _I, [_P, _SZ, _P]),
+    ("lutgemm_gemv", _I, [ctypes.POINTER(lutgemm_weight), _P, _P, _P, _SZ, _P]),
+    ("lutgemm_gemm_batched", _I, [ctypes.POINTER(lutgemm_weight), _P, _I, _P, _P, _SZ, _P]),
+    ("lutgemm_gemm_batched_f32", _I, [ctypes.POINTER(lutgemm_weight), _P, _I, _P, _P, _SZ, _P]),
+    ("lutgemm_host_workspace_bytes", _SZ, [_I, _I, _I]),
+    ("lutgemm_gemm_host", _I, [ctypes.POINTER(lutgemm_weight), _P, _I, _P, _P, _SZ, _P]),
+    ("lutgemm_tp_unique_id", _I, [_P]),
+    ("lutgemm_tp_init", _I, [_I, _I, _P, ctypes.POINTER(_P)]),
+    ("lutgemm_tp_workspace_bytes", _SZ, [_P, _I, _I, _I, _I]),
+    ("lutgemm_tp_linear", _I, [_P, _I, ctypes.POINTER(lutgemm_weight), _P, _I, _P, _P, _SZ, _P]),
+    ("lutgemm_tp_destroy", _I, [_P]),
+    ("lutgemm_tp_rank", _I, [_P]),
+    ("lutgemm_tp_nranks", _I, [_P]),
+]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built (run `python -c 'import __graft_entry__ as g; g.build()'`); "
+                          "there is no CPU fallback for the LUT-GEMM path")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def _check(fn: str, status: int):
+    if status != OK:
+        raise LutgemmError(fn, status, lib.lutgemm_last_error().decode(errors="replace"))
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream=None) -> int:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def lutgemm_packed_bytes(m: int, n: int, q: int, g: int, has_offset: bool) -> tuple[int, int, int]:
+    a, b, c = _SZ(), _SZ(), _SZ()
+    _check("lutgemm_packed_bytes",
+           lib.lutgemm_packed_bytes(m, n, q, g, int(has_offset), ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+    return a.value, b.value, c.value
+
+
+@dataclass
+class PackedBCQ:
+    """A packed weight resident on the device (kernel-native layout); the
+    three torch tensors own the memory, ``struct`` is the C view of them."""
+    m: int
+    n: int
+    q: int
+    g: int
+    has_offset: bool
+    planes: torch.Tensor
+    alpha: torch.Tensor
+    offset: torch.Tensor | None
+    struct: lutgemm_weight = field(default=None)
+
+    @classmethod
+    def empty(cls, m, n, q, g, has_offset, device) -> "PackedBCQ":
+        pb, ab, ob = lutgemm_packed_bytes(m, n, q, g, has_offset)
+        planes = torch.empty(pb, dtype=torch.uint8, device=device)
+        alpha = torch.empty(ab // 2, dtype=torch.float16, device=device)
+        offset = torch.empty(ob // 2, dtype=torch.float16, device=device) if has_offset else None
+        w = cls(m, n, q, g, has_offset, planes, alpha, offset)
+        w.struct = lutgemm_weight(m, n, q, g, int(has_offset), 0, planes.data_ptr(), alpha.data_ptr(),
+                                  _ptr(offset))
+        return w
+
+    def nbytes(self) -> int:
+        return self.planes.numel() + 2 * self.alpha.numel() + (2 * self.offset.numel() if self.offset is not None else 0)
+
+
+def lutgemm_pack_bcq(planes: torch.Tensor, alpha: torch.Tensor, offset: torch.Tensor | None, n: int, g: int,
+                     stream=None) -> PackedBCQ:
+    """Canonical BCQ (device tensors: planes int32/uint32 [q][m][n/32], alpha fp16
+    [m][n/g][q], offset fp16 [m][n/g] or None) -> PackedBCQ."""
+    q, m = int(planes.shape[0]), int(planes.shape[1])
+    for t in (planes, alpha, offset):
+        if t is not None and (not t.is_cuda or not t.is_contiguous()):
+            raise ValueError("pack sources must be contiguous CUDA tensors")
+    w = PackedBCQ.empty(m, n, q, g, offset is not None, planes.device)
+    src = lutgemm_pack_src(SRC_BCQ, m, n, q, g, 0, planes.data_ptr(), alpha.data_ptr(), _ptr(offset), None, None,
+                           None)
+    _check("lutgemm_pack_bcq", lib.lutgemm_pack_bcq(ctypes.byref(src), ctypes.byref(w.struct), _stream(stream)))
+    return w
+
+
+def lutgemm_pack_uniform(codes: torch.Tensor, scale: torch.Tensor, zero: torch.Tensor, q: int, g: int,
+                         stream=None) -> PackedBCQ:
+    """Uniform codes (uint8 [m][n]), s and z_hat (fp16 [m][n/g]) -> extended BCQ (App. C)."""
+    m, n = int(codes.shape[0]), int(codes.shape[1])
+    for t in (codes, scale, zero):
+        if not t.is_cuda or not t.is_contiguous():
+            raise ValueError("pack sources must be contiguous CUDA tensors")
+    w = PackedBCQ.empty(m, n, q, g, True, codes.device)
+    src = lutgemm_pack_src(SRC_UNIFORM, m, n, q, g, 0, None, None, None, codes.data_ptr(), scale.data_ptr(),
+                           zero.data_ptr())
+    _check("lutgemm_pack_bcq", lib.lutgemm_pack_bcq(ctypes.byref(src), ctypes.byref(w.struct), _stream(stream)))
+    return w
+
+
+def lutgemm_unpack_bcq(w: PackedBCQ, stream=None):
+    """Native -> canonical (planes int32 [q][m][n/32], alpha fp16 [m][G][q], offset fp16 [m][G] | None)."""
+    dev = w.planes.device
+    G = w.n // w.g
+    planes = torch.empty((w.q, w.m, w.n // 32), dtype=torch.int32, device=dev)
+    alpha = torch.empty((w.m, G, w.q), dtype=torch.float16, device=dev)
+    offset = torch.empty((w.m, G), dtype=torch.float16, device=dev) if w.has_offset else None
+    _check("lutgemm_unpack_bcq", lib.lutgemm_unpack_bcq(ctypes.byref(w.struct), planes.data_ptr(), alpha.data_ptr(),
+                                                        _ptr(offset), _stream(stream)))
+    return planes, alpha, offset
+
+
+def lutgemm_workspace_bytes(m: int, n: int, b: int = 1) -> int:
+    return int(lib.lutgemm_workspace_bytes(m, n, b))
+
+
+def make_workspace(nbytes: int, device, stream=None) -> torch.Tensor:
+    ws = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=device)
+    _check("lutgemm_workspace_init", lib.lutgemm_workspace_init(ws.data_ptr(), ws.numel(), _stream(stream)))
+    return ws
+
+
+def lutgemm_gemv(w: PackedBCQ, x: torch.Tensor, y: torch.Tensor | None = None, ws: torch.Tensor | None = None,
+                 stream=None) -> torch.Tensor:
+    """y[m] (fp16) = W x[n] (fp16)."""
+    if y is None:
+        y = torch.empty(w.m, dtype=torch.float16, device=x.device)
+    if ws is None:
+        ws = make_workspace(lutgemm_workspace_bytes(w.m, w.n, 1), x.device, stream)
+    _check("lutgemm_gemv", lib.lutgemm_gemv(ctypes.byref(w.struct), x.data_ptr(), y.data_ptr(), ws.data_ptr(),
+                                            ws.numel(), _stream(stream)))
+    return y
+
+
+def lutgemm_gemm_batched(w: PackedBCQ, X: torch.Tensor, Y: torch.Tensor | None = None,
+                         ws: torch.Tensor | None = None, stream=None, f32: bool = False) -> torch.Tensor:
+    """Y[b][m] = X[b][n] W^T, 1 <= b <= 32 (fp16 out, or fp32 with f32=True)."""
+    b = int(X.shape[0])
+    if Y is None:
+        Y = torch.empty((b, w.m), dtype=torch.float32 if f32 else torch.float16, device=X.device)
+    if ws is None:
+        ws = make_workspace(lutgemm_workspace_bytes(w.m, w.n, b), X.device, stream)
+    fn = lib.lutgemm_gemm_batched_f32 if f32 else lib.lutgemm_gemm_batched
+    _check("lutgemm_gemm_batched", fn(ctypes.byref(w.struct), X.data_ptr(), b, Y.data_ptr(), ws.data_ptr(),
+                                      ws.numel(), _stream(stream)))
+    return Y
+
+
+def lutgemm_host_workspace_bytes(m: int, n: int, b: int = 1) -> int:
+    return int(lib.lutgemm_host_workspace_bytes(m, n, b))
+
+
+def lutgemm_gemm_host(w: PackedBCQ, X_host: torch.Tensor, Y_host: torch.Tensor, ws: torch.Tensor, stream=None):
+    """End-to-end: host X [b][n] -> device -> LUT-GEMM -> host Y [b][m] (synchronous)."""
+    b = int(X_host.shape[0]) if X_host.dim() == 2 else 1
+    _check("lutgemm_gemm_host", lib.lutgemm_gemm_host(ctypes.byref(w.struct), X_host.data_ptr(), b, Y_host.data_ptr(),
+                                                      ws.data_ptr(), ws.numel(), _stream(stream)))
+    return Y_host
+
+
+# ---------------------------------------------------------------------------
+# tensor parallelism
+# ---------------------------------------------------------------------------
+
+class TPComm:
+    """NCCL communicator for lutgemm_tp_linear; the unique id travels over the
+    caller's torch.distributed process group (plumbing only)."""
+
+    def __init__(self, rank: int, world: int, group=None, device=None):
+        import torch.distributed as dist
+        idbuf = (ctypes.c_uint8 * 128)()
+        if rank == 0:
+            _check("lutgemm_tp_unique_id", lib.lutgemm_tp_unique_id(ctypes.cast(idbuf, _P)))
+        backend = dist.get_backend(group)
+        dev = device if (backend == "nccl") else "cpu"
+        t = torch.tensor(list(bytes(idbuf)), dtype=torch.uint8, device=dev)
+        dist.broadcast(t, src=0, group=group)
+        raw = bytes(t.cpu().tolist())
+        ctypes.memmove(idbuf, raw, 128)
+        h = _P()
+        _check("lutgemm_tp_init", lib.lutgemm_tp_init(world, rank, ctypes.cast(idbuf, _P), ctypes.byref(h)))
+        self.handle = h
+        self.rank, self.world = rank, world
+
+    def workspace_bytes(self, mode: int, m_shard: int, n_shard: int, b: int) -> int:
+        return int(lib.lutgemm_tp_workspace_bytes(self.handle, mode, m_shard, n_shard, b))
+
+    def linear(self, mode: int, shard: PackedBCQ, x: torch.Tensor, y: torch.Tensor, ws: torch.Tensor, stream=None):
+        b = int(x.shape[0]) if x.dim() == 2 else 1
+        _check("lutgemm_tp_linear", lib.lutgemm_tp_linear(self.handle, mode, ctypes.byref(shard.struct), x.data_ptr(),
+                                                          b, y.data_ptr(), ws.data_ptr(), ws.numel(),
+                                                          _stream(stream)))
+        return y
+
+    def close(self):
+        if self.handle:
+            _check("lutgemm_tp_destroy", lib.lutgemm_tp_destroy(self.handle))
+            self.handle = None

@@ -1,0 +1,75 @@
+"""CPU-only checks of the boundary: the C-ABI library loads, exports every
+symbol include/lutgemm.h declares, and its host-side logic (sizes, argument
+validation) behaves as documented.  No compute call needs a GPU here."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "lutgemm.h")
+
+
+def _declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(lutgemm_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_2206_09557_b200.lutgemm as B
+    lib = ctypes.CDLL(B.LIB_PATH)
+    names = _declared_functions()
+    assert len(names) >= 15
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    # and the binding wraps exactly the declared set
+    assert sorted(n for n, _, _ in B.SIGNATURES) == names
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+    import paper_2206_09557_b200.lutgemm as B
+    out = subprocess.run(["cuobjdump", "--list-elf", B.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert all("sm_100a" in line for line in out.splitlines() if "ELF" in line)
+
+
+def test_abi_version_and_sizes():
+    import paper_2206_09557_b200 as L
+    from paper_2206_09557_b200.lutgemm import lib
+    assert lib.lutgemm_abi_version() == 1
+    # planes = m4*q*n/8, alpha = m4*(n/g)*q*2, offset = m4*(n/g)*2 (layout.cuh)
+    assert L.lutgemm_packed_bytes(49152, 12288, 3, 128, False) == (226492416, 28311552, 0)
+    assert L.lutgemm_packed_bytes(22013, 8192, 4, 128, True) == (22016 * 4 * 1024, 22016 * 64 * 4 * 2, 22016 * 64 * 2)
+    # workspace: counters (ceil(RQ/16) u32, 256-B rounded) + S*b*m4 fp32 partials
+    ws = L.lutgemm_workspace_bytes(49152, 12288, 1)
+    assert ws == 3072 + 12 * 49152 * 4
+    assert L.lutgemm_workspace_bytes(49152, 12288, 4) == 3072 + 12 * 4 * 49152 * 4
+
+
+@pytest.mark.parametrize("m,n,q,g", [(0, 64, 3, 32), (8, 48, 3, 48), (8, 64, 0, 32), (8, 64, 9, 32),
+                                     (8, 64, 3, 16), (8, 96, 3, 64), (8, 64, 3, 96)])
+def test_invalid_shapes_rejected(m, n, q, g):
+    import paper_2206_09557_b200 as L
+    with pytest.raises(L.LutgemmError) as ei:
+        L.lutgemm_packed_bytes(m, n, q, g, False)
+    assert ei.value.status == 1
+    assert "must" in str(ei.value)
+
+
+def test_gemv_argument_validation_without_gpu():
+    """Validation happens before any device work: NULL/misaligned/small-ws
+    arguments are rejected on a CPU-only host too."""
+    from paper_2206_09557_b200.lutgemm import lib, lutgemm_weight
+    w = lutgemm_weight(64, 64, 3, 32, 0, 0, 4096, 8192, None)
+    st = lib.lutgemm_gemv(ctypes.byref(w), 4096 + 2, 8192, 16384, 1 << 20, None)
+    assert st == 2 and b"x must be 16-byte aligned" in lib.lutgemm_last_error()
+    st = lib.lutgemm_gemv(ctypes.byref(w), 4096, 8192, 16384, 16, None)
+    assert st == 3 and b"workspace" in lib.lutgemm_last_error()
+    st = lib.lutgemm_gemm_batched(ctypes.byref(w), 4096, 33, 8192, 16384, 1 << 20, None)
+    assert st == 1
+    w.has_offset = 1
+    st = lib.lutgemm_gemv(ctypes.byref(w), 4096, 8192, 16384, 1 << 20, None)
+    assert st == 1 and b"offset" in lib.lutgemm_last_error()
