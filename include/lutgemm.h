@@ -26,10 +26,12 @@
  *  - The library is stateless except for an explicit TP communicator and the
  *    thread-local error text; calls on distinct outputs/workspaces are
  *    thread-safe.
- *  - Supported shapes on the GPU path: n % 32 == 0, g % 32 == 0, n % g == 0
- *    (g == n is row-wise, P:L496 '-' / P:L392 "g=m"), 1 <= q <= 8, m >= 1,
+ *  - Supported shapes on the GPU path: n % 32 == 0, n % g == 0 and
+ *    g in {32, 64, 128, 256, 512, 1024} or g a multiple of 1024 or g == n
+ *    (g == n is row-wise, P:L496 '-' / P:L392 "g=m"); 1 <= q <= 8, m >= 1,
  *    1 <= b <= 32.  Anything else returns LUTGEMM_ERR_INVALID_ARG (DESIGN.md
- *    reading R13: the paper does not define chunks straddling a group).
+ *    reading R13: the paper does not define chunks straddling a group; the
+ *    power-of-two rule keeps every group inside one 1024-column LUT slice).
  *  - Requires an sm_100 device (B200); otherwise LUTGEMM_ERR_UNSUPPORTED.
  */
 #ifndef LUTGEMM_H_
@@ -54,20 +56,16 @@ typedef enum {
   LUTGEMM_ERR_UNSUPPORTED = 6  /* current device is not sm_100 */
 } lutgemm_status;
 
-/* A packed weight in the kernel-native layout (opaque byte order; see
- * DESIGN.md "Data layout in HBM").  The struct itself lives on the host; the
- * three buffers live on the device and are owned by the caller.
- *   planes : lutgemm_packed_bytes().planes bytes, 16-byte aligned
- *   alpha  : lutgemm_packed_bytes().alpha bytes, 16-byte aligned (fp16)
- *   offset : lutgemm_packed_bytes().offset bytes, 16-byte aligned (fp16), or
- *            NULL when has_offset == 0 (z = 0). */
+/* A packed weight in the kernel-native layout: ONE device buffer holding the
+ * bit-planes, scales and (if has_offset) biases as a slice-major stream of
+ * per-row-quad records (opaque byte order).
+ * The struct lives on the host; `data` (lutgemm_packed_bytes() bytes,
+ * 16-byte aligned) lives on the device and is owned by the caller. */
 typedef struct {
   int32_t m, n, q, g;
-  int32_t has_offset;
+  int32_t has_offset; /* 1: extended BCQ with bias z (Eq. 3); 0: z = 0 */
   int32_t reserved;
-  void* planes;
-  void* alpha;
-  void* offset;
+  void* data;
 } lutgemm_weight;
 
 enum { LUTGEMM_SRC_BCQ = 0, LUTGEMM_SRC_UNIFORM = 1 };
@@ -106,16 +104,15 @@ int lutgemm_abi_version(void);
 /* Thread-local text for the last non-OK status returned on this thread. */
 const char* lutgemm_last_error(void);
 
-/* Byte sizes of the three native buffers for an (m, n, q, g) weight.
- * offset_bytes is 0 when has_offset == 0.  Pure host computation. */
-lutgemm_status lutgemm_packed_bytes(int m, int n, int q, int g, int has_offset,
-                                    size_t* planes_bytes, size_t* alpha_bytes,
-                                    size_t* offset_bytes);
+/* Byte size of the native buffer of an (m, n, q, g, has_offset) weight:
+ * m4*n*q/8 bits + the stored scales/biases (+ 16-byte record padding), with
+ * m4 = 4*ceil(m/4).  Pure host computation. */
+lutgemm_status lutgemm_packed_bytes(int m, int n, int q, int g, int has_offset, size_t* bytes);
 
-/* Repack a canonical BCQ or uniform source into dst's native buffers (which
- * the caller allocated with lutgemm_packed_bytes sizes and set in dst).  The
- * call fills dst->m, n, q, g, has_offset (has_offset = 1 for UNIFORM, and for
- * BCQ iff src->offset != NULL).  Offline step (App. C "two-step methodology",
+/* Repack a canonical BCQ or uniform source into dst->data (which the caller
+ * allocated with lutgemm_packed_bytes(..., has_offset) bytes, has_offset = 1
+ * for UNIFORM, and for BCQ iff src->offset != NULL).  The call fills dst->m,
+ * n, q, g, has_offset.  Offline step (App. C "two-step methodology",
  * P:L615-620); asynchronous on `stream`. */
 lutgemm_status lutgemm_pack_bcq(const lutgemm_pack_src* src, lutgemm_weight* dst, void* stream);
 
@@ -160,6 +157,16 @@ lutgemm_status lutgemm_gemm_batched_f32(const lutgemm_weight* w, const uint16_t*
 size_t lutgemm_host_workspace_bytes(int m, int n, int b);
 lutgemm_status lutgemm_gemm_host(const lutgemm_weight* w, const uint16_t* X_host, int b, uint16_t* Y_host,
                                  void* ws, size_t ws_bytes, void* stream);
+
+/* Tracing (debug; not for the hot path).  When enabled, every subsequent
+ * product launch records a per-CTA %globaltimer timeline into a library-owned
+ * device buffer (8 u64 per CTA, up to 1024 CTAs, last launch wins):
+ * [0] CTA start, [1] x slice staged, [2] first LUT built, [3] warp 0 done with
+ * the first segment, [4] all warps done with it, [5]/[6] the same for the last
+ * segment (6 is also the CTA end), [7] SM id.  lutgemm_trace_read copies up to
+ * n values to host memory (synchronous) and returns how many it copied. */
+lutgemm_status lutgemm_trace_enable(int on);
+size_t lutgemm_trace_read(uint64_t* host, size_t n);
 
 /* ---------------- Tensor parallelism over NCCL (NVLink / NVSwitch) ----------------
  * The paper runs LUT-GEMM tensor-parallel on 1/2/4/8 GPUs (P:L378-385,

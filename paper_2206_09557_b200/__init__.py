@@ -14,6 +14,8 @@ from .lutgemm import (  # noqa: F401
     TP_ROWS_LOCAL,
     lutgemm_gemm_batched,
     lutgemm_gemm_host,
+    lutgemm_trace_enable,
+    lutgemm_trace_read,
     lutgemm_gemv,
     lutgemm_host_workspace_bytes,
     lutgemm_pack_bcq,

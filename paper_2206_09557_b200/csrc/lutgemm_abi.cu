@@ -32,8 +32,10 @@ lutgemm_status check_shape(int m, int n, int q, int g) {
   if (m < 1) return fail(LUTGEMM_ERR_INVALID_ARG, "m=%d must be >= 1", m);
   if (n < 32 || n % 32) return fail(LUTGEMM_ERR_INVALID_ARG, "n=%d must be a positive multiple of 32", n);
   if (q < 1 || q > 8) return fail(LUTGEMM_ERR_INVALID_ARG, "q=%d must be in [1, 8]", q);
-  if (g < 32 || g % 32 || n % g)
-    return fail(LUTGEMM_ERR_INVALID_ARG, "g=%d must be a multiple of 32 dividing n=%d (g=n is row-wise)", g, n);
+  const bool g_ok = (g >= 32 && g <= 1024 && (1024 % g) == 0) || (g > 1024 && (g % 1024 == 0 || g == n));
+  if (!g_ok || n % g)
+    return fail(LUTGEMM_ERR_INVALID_ARG,
+                "g=%d must divide n=%d and be one of 32..1024 (power of two), a multiple of 1024, or n", g, n);
   if ((long long)m * (n / 32) >= (1LL << 40)) return fail(LUTGEMM_ERR_INVALID_ARG, "shape too large");
   return LUTGEMM_OK;
 }
@@ -63,10 +65,9 @@ lutgemm_status check_weight(const lutgemm_weight* w) {
   if (!w) return fail(LUTGEMM_ERR_INVALID_ARG, "weight is NULL");
   lutgemm_status st = check_shape(w->m, w->n, w->q, w->g);
   if (st != LUTGEMM_OK) return st;
-  if (!w->planes || !w->alpha) return fail(LUTGEMM_ERR_INVALID_ARG, "weight planes/alpha is NULL");
-  if (w->has_offset && !w->offset) return fail(LUTGEMM_ERR_INVALID_ARG, "has_offset=1 but offset is NULL");
-  if (!aligned(w->planes, 16) || !aligned(w->alpha, 16) || (w->has_offset && !aligned(w->offset, 16)))
-    return fail(LUTGEMM_ERR_MISALIGNED, "weight buffers must be 16-byte aligned");
+  if (!w->data) return fail(LUTGEMM_ERR_INVALID_ARG, "weight data is NULL");
+  if (w->has_offset != 0 && w->has_offset != 1) return fail(LUTGEMM_ERR_INVALID_ARG, "has_offset must be 0 or 1");
+  if (!aligned(w->data, 16)) return fail(LUTGEMM_ERR_MISALIGNED, "weight data must be 16-byte aligned");
   return LUTGEMM_OK;
 }
 
@@ -80,13 +81,12 @@ lutgemm_status product(const lutgemm_weight* w, const uint16_t* X, int b, uint16
   if (!aligned(ws, 16)) return fail(LUTGEMM_ERR_MISALIGNED, "ws must be 16-byte aligned");
   if (Y && !aligned(Y, 2)) return fail(LUTGEMM_ERR_MISALIGNED, "y must be 2-byte aligned");
   if (Yf && !aligned(Yf, 4)) return fail(LUTGEMM_ERR_MISALIGNED, "yf must be 4-byte aligned");
-  const lg::Shape sh = lg::make_shape(w->m, w->n, w->q, w->g);
+  const lg::Shape sh = lg::make_shape(w->m, w->n, w->q, w->g, w->has_offset);
   const size_t need = lg::workspace_bytes(sh, b);
   if (ws_bytes < need) return fail(LUTGEMM_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, need);
   st = check_device();
   if (st != LUTGEMM_OK) return st;
-  cudaError_t e = lg::run_product(sh, w->planes, w->alpha, w->has_offset ? w->offset : nullptr, X, b, Y, Yf, ws,
-                                  static_cast<cudaStream_t>(stream));
+  cudaError_t e = lg::run_product(sh, w->data, X, b, Y, Yf, ws, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "LUT-GEMM kernel launch");
   return LUTGEMM_OK;
 }
@@ -99,14 +99,11 @@ int lutgemm_abi_version(void) { return LUTGEMM_ABI_VERSION; }
 
 const char* lutgemm_last_error(void) { return g_err; }
 
-lutgemm_status lutgemm_packed_bytes(int m, int n, int q, int g, int has_offset, size_t* planes_bytes,
-                                    size_t* alpha_bytes, size_t* offset_bytes) {
+lutgemm_status lutgemm_packed_bytes(int m, int n, int q, int g, int has_offset, size_t* bytes) {
   lutgemm_status st = check_shape(m, n, q, g);
   if (st != LUTGEMM_OK) return st;
-  const lg::Shape sh = lg::make_shape(m, n, q, g);
-  if (planes_bytes) *planes_bytes = lg::planes_bytes(sh);
-  if (alpha_bytes) *alpha_bytes = lg::alpha_elems(sh) * 2u;
-  if (offset_bytes) *offset_bytes = has_offset ? lg::offset_elems(sh) * 2u : 0u;
+  if (!bytes) return fail(LUTGEMM_ERR_INVALID_ARG, "bytes is NULL");
+  *bytes = lg::packed_bytes(lg::make_shape(m, n, q, g, has_offset));
   return LUTGEMM_OK;
 }
 
@@ -123,24 +120,20 @@ lutgemm_status lutgemm_pack_bcq(const lutgemm_pack_src* src, lutgemm_weight* dst
     return fail(LUTGEMM_ERR_INVALID_ARG, "BCQ source needs planes and alpha");
   }
   const int has_offset = uniform ? 1 : (src->offset != nullptr);
-  if (!dst->planes || !dst->alpha || (has_offset && !dst->offset))
-    return fail(LUTGEMM_ERR_INVALID_ARG, "destination buffers not set");
-  if (!aligned(dst->planes, 16) || !aligned(dst->alpha, 16) || (has_offset && !aligned(dst->offset, 16)))
-    return fail(LUTGEMM_ERR_MISALIGNED, "destination buffers must be 16-byte aligned");
+  if (!dst->data) return fail(LUTGEMM_ERR_INVALID_ARG, "destination buffer not set");
+  if (!aligned(dst->data, 16)) return fail(LUTGEMM_ERR_MISALIGNED, "destination buffer must be 16-byte aligned");
   if ((src->planes && !aligned(src->planes, 4)) || (src->alpha && !aligned(src->alpha, 2)) ||
       (src->offset && !aligned(src->offset, 2)) || (src->scale && !aligned(src->scale, 2)) ||
       (src->zero && !aligned(src->zero, 2)))
     return fail(LUTGEMM_ERR_MISALIGNED, "source buffers must be element-aligned");
   st = check_device();
   if (st != LUTGEMM_OK) return st;
-  const lg::Shape sh = lg::make_shape(src->m, src->n, src->q, src->g);
+  const lg::Shape sh = lg::make_shape(src->m, src->n, src->q, src->g, has_offset);
   cudaError_t e;
   if (uniform)
-    e = lg::run_pack_uniform(sh, src->codes, src->scale, src->zero, dst->planes, dst->alpha, dst->offset,
-                             static_cast<cudaStream_t>(stream));
+    e = lg::run_pack_uniform(sh, src->codes, src->scale, src->zero, dst->data, static_cast<cudaStream_t>(stream));
   else
-    e = lg::run_pack_bcq(sh, src->planes, src->alpha, src->offset, dst->planes, dst->alpha, dst->offset,
-                         static_cast<cudaStream_t>(stream));
+    e = lg::run_pack_bcq(sh, src->planes, src->alpha, src->offset, dst->data, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "pack kernel launch");
   dst->m = src->m;
   dst->n = src->n;
@@ -148,7 +141,6 @@ lutgemm_status lutgemm_pack_bcq(const lutgemm_pack_src* src, lutgemm_weight* dst
   dst->g = src->g;
   dst->has_offset = has_offset;
   dst->reserved = 0;
-  if (!has_offset) dst->offset = nullptr;
   return LUTGEMM_OK;
 }
 
@@ -159,16 +151,15 @@ lutgemm_status lutgemm_unpack_bcq(const lutgemm_weight* w, uint32_t* planes, uin
   if (offset && !w->has_offset) return fail(LUTGEMM_ERR_INVALID_ARG, "weight has no offset to unpack");
   st = check_device();
   if (st != LUTGEMM_OK) return st;
-  const lg::Shape sh = lg::make_shape(w->m, w->n, w->q, w->g);
-  cudaError_t e = lg::run_unpack(sh, w->planes, w->alpha, w->has_offset ? w->offset : nullptr, planes, alpha,
-                                 offset, static_cast<cudaStream_t>(stream));
+  const lg::Shape sh = lg::make_shape(w->m, w->n, w->q, w->g, w->has_offset);
+  cudaError_t e = lg::run_unpack(sh, w->data, planes, alpha, offset, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "unpack kernel launch");
   return LUTGEMM_OK;
 }
 
 size_t lutgemm_workspace_bytes(int m, int n, int b) {
   if (m < 1 || n < 32 || b < 1) return 0;
-  const lg::Shape sh = lg::make_shape(m, n, 1, n);
+  const lg::Shape sh = lg::make_shape(m, n, 1, n, 0);
   return lg::workspace_bytes(sh, b);
 }
 
@@ -226,6 +217,15 @@ lutgemm_status lutgemm_gemm_host(const lutgemm_weight* w, const uint16_t* X_host
   e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
   return LUTGEMM_OK;
+}
+
+lutgemm_status lutgemm_trace_enable(int on) {
+  lg::trace_enable(on);
+  return LUTGEMM_OK;
+}
+
+size_t lutgemm_trace_read(uint64_t* host, size_t n) {
+  return lg::trace_read(reinterpret_cast<unsigned long long*>(host), n);
 }
 
 }  // extern "C"

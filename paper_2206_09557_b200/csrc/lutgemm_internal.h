@@ -11,33 +11,40 @@
 namespace lg {
 
 struct KParams {
-  const uint8_t* planes;
-  const __half* alpha;
-  const __half* offset;
+  const uint8_t* data;   // packed record stream (layout.cuh)
   const __half* x;   // [b][n]
   __half* y;         // [b][m] fp16 output (or null)
   float* yf;         // [b][m] fp32 output (or null)
   float* partial;    // [S][b][m4] split-K partials
-  unsigned* counters;
+  unsigned* counters;  // [S] GEMV chunk counters (zero between launches)
   Shape sh;
   int b;
   int bl;            // log2 of the table-bank count B >= b
+  int pf_steps;      // GEMV: L2 prefetch distance in 16-quad steps
+  int xmode;         // experiment knob (0 default)
   long long items;
+  unsigned long long* trace;  // optional per-CTA timeline (kTraceSlots u64 per CTA), or null
 };
 
-size_t counters_bytes(const Shape& sh);
+constexpr int kTraceSlots = 8;
+// tracing (debug): enable a per-CTA %globaltimer timeline of the next launches
+void trace_enable(int on);
+size_t trace_read(unsigned long long* host, size_t n);
+
 size_t workspace_bytes(const Shape& sh, int b);
 
-// y (fp16) or yf (fp32) [b][m] = X [b][n] W^T.  One kernel launch.
-cudaError_t run_product(const Shape& sh, const void* planes, const void* alpha, const void* offset,
-                        const uint16_t* x, int b, uint16_t* y, float* yf, void* ws, cudaStream_t st);
+// y (fp16) or yf (fp32) [b][m] = X [b][n] W^T.  Two launches chained with
+// programmatic dependent launch: the LUT kernel (split-K partials), then the
+// fixed-order cross-slice reduction.
+cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, int b, uint16_t* y, float* yf,
+                        void* ws, cudaStream_t st);
 
 cudaError_t run_pack_bcq(const Shape& sh, const uint32_t* planes, const uint16_t* alpha, const uint16_t* offset,
-                         void* dplanes, void* dalpha, void* doffset, cudaStream_t st);
+                         void* dst, cudaStream_t st);
 cudaError_t run_pack_uniform(const Shape& sh, const uint8_t* codes, const uint16_t* scale, const uint16_t* zero,
-                             void* dplanes, void* dalpha, void* doffset, cudaStream_t st);
-cudaError_t run_unpack(const Shape& sh, const void* dplanes, const void* dalpha, const void* doffset,
-                       uint32_t* planes, uint16_t* alpha, uint16_t* offset, cudaStream_t st);
+                             void* dst, cudaStream_t st);
+cudaError_t run_unpack(const Shape& sh, const void* src, uint32_t* planes, uint16_t* alpha, uint16_t* offset,
+                       cudaStream_t st);
 
 // TP helpers
 cudaError_t run_cast_f32_f16(const float* src, uint16_t* dst, size_t count, cudaStream_t st);

@@ -18,18 +18,26 @@
 //    -> every lookup instruction of a warp hits 32 distinct banks whatever the
 //    keys are (bank = lane), and key -> address is ONE byte permute (PRMT)
 //    because the LUT sits on a 64 KB boundary of the shared window;
-//  * packed planes streamed HBM -> registers with 128-bit coalesced loads
-//    (L1::no_allocate), a PD-deep register ring prefetching row quads;
+//  * the weight is one slice-major record stream (layout.cuh); one thread
+//    keeps a bulk L2 prefetch (TMA engine, UBLKPF) several row-quad steps
+//    ahead of the warps, whose 128-bit loads (L1::no_allocate) then hit L2;
+//    a PD-deep register ring overlaps those loads with the lookups;
 //  * the activation slice is staged into shared memory by the bulk-copy
 //    (TMA) engine, double-buffered one segment ahead;
-//  * per-row partials reduced in registers by a 6-shuffle transpose-reduce,
-//    written to an fp32 split-K workspace, and summed in slice order by the
-//    last CTA to finish each row block (deterministic, one launch).
+//  * lookups summed and scaled with packed f32x2 adds/FMAs (FADD2/FFMA2),
+//    two rows per instruction;
+//  * per-row partials reduced across lanes by a 6-shuffle transpose-reduce and
+//    written to an fp32 split-K workspace; a small second kernel, chained by
+//    programmatic dependent launch (PDL), sums the slices in fixed order
+//    (deterministic) and rounds y to fp16.  The LUT kernel streams its first
+//    weights before griddepcontrol.wait, so back-to-back products overlap.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "layout.cuh"
 #include "lutgemm_internal.h"
@@ -39,10 +47,10 @@ namespace lg {
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-constexpr int kBlkQuads = 64;      // GEMV arrival-counter block: 64 row quads = 256 rows
-constexpr int kQPW = 8;            // batched: row quads per warp per work item
-constexpr int kMiscBytes = 8192;   // x double buffer (2 x 2 KB) + mbarriers + flags
-constexpr int kSmemBytes = 3 * 65536;  // LUT (128 KB) on a 64 KB boundary + misc, any base
+constexpr int kQPW = 8;                // batched: row quads per warp per work item
+constexpr int kMiscBytes = 8192;       // x double buffer (2 x 2 KB) + mbarriers + flags
+constexpr int kSmemBytes = 3 * 65536;  // LUT (128 KB) on a 64 KB boundary + misc, for any base
+constexpr int kPfSteps = 8;            // GEMV: L2 prefetch distance in 16-quad steps
 constexpr unsigned kFull = 0xffffffffu;
 
 struct SmemMap {
@@ -67,7 +75,7 @@ __device__ __forceinline__ uint32_t table_offset(int l, int j) {
 
 // Build entries [64h, 64h+64) of one table T[k] = sum_j (2 bit_j(k) - 1) x_j
 // (mu = 8, key bit j <-> column 8t+j, R3).  T[k] = L[k&15] + H[k>>4]
-// with L over x0..x3 and H over x4..x7: 1 add per entry (Eq. 2's C_build).
+// with L over x0..x3 and H over x4..x7: one add per entry (Eq. 2's C_build).
 __device__ __forceinline__ void build_table_part(uint32_t tbl, const __half* xc, int h) {
   const uint4 raw = *reinterpret_cast<const uint4*>(xc);
   const float2 x01 = h2_to_f2(raw.x), x23 = h2_to_f2(raw.y), x45 = h2_to_f2(raw.z), x67 = h2_to_f2(raw.w);
@@ -87,27 +95,39 @@ __device__ __forceinline__ void build_table_part(uint32_t tbl, const __half* xc,
   }
 }
 
-// Four lookups (chunk steps j = 0..3 of one packed word = 4 keys) summed.
-// lc = LUT[31:16] | (4l+128) << 8 | 4l ; PRMT puts key byte j in bits 8..15.
-__device__ __forceinline__ float lut4(uint32_t w, uint32_t lc) {
-  const float v0 = lds_f32<0>(prmt<0x7604>(w, lc));
-  const float v1 = lds_f32<0>(prmt<0x7615>(w, lc));
-  const float v2 = lds_f32<65536>(prmt<0x7624>(w, lc));
-  const float v3 = lds_f32<65536>(prmt<0x7635>(w, lc));
-  return (v0 + v1) + (v2 + v3);
+// Lookup of key byte J of word w: PRMT places the byte in bits 8..15 next to
+// the lane constant lc = LUT[31:16] | (4l+128) << 8 | 4l.
+// MODE != 0 are measurement variants (tools/kernel_probe): 1 = no LDS.
+template <int J, int MODE = 0>
+__device__ __forceinline__ float lut1(uint32_t w, uint32_t lc) {
+  constexpr uint32_t kSel = ((J & 1) ? 0x7605u : 0x7604u) | ((uint32_t)J << 4);
+  if (MODE == 1) return __uint_as_float(prmt<kSel>(w, lc) & 0x3fffffffu);
+  return lds_f32<(J >> 1) * 65536>(prmt<kSel>(w, lc));
 }
 
-// Transpose-reduce of 4 per-lane row partials over the 32 lanes; returns the
-// full sum of row (lane >> 3) & 3 (valid in lanes 0, 8, 16, 24).
-__device__ __forceinline__ float reduce4(const float acc[4], int lane) {
+// sum over the 4 keys of word wa (row a) and of word wb (row b), as the pair (a, b)
+template <int MODE = 0>
+__device__ __forceinline__ f32x2 lut4x2(uint32_t wa, uint32_t wb, uint32_t lc) {
+  const f32x2 p0 = pack2(lut1<0, MODE>(wa, lc), lut1<0, MODE>(wb, lc));
+  const f32x2 p1 = pack2(lut1<1, MODE>(wa, lc), lut1<1, MODE>(wb, lc));
+  const f32x2 p2 = pack2(lut1<2, MODE>(wa, lc), lut1<2, MODE>(wb, lc));
+  const f32x2 p3 = pack2(lut1<3, MODE>(wa, lc), lut1<3, MODE>(wb, lc));
+  return add2(add2(p0, p1), add2(p2, p3));
+}
+
+// Transpose-reduce of the 4 per-lane row partials (pairs (0,1), (2,3)) over
+// the 32 lanes; returns the full sum of row (lane >> 3) & 3 (valid in lanes
+// 0, 8, 16, 24).
+__device__ __forceinline__ float reduce4(f32x2 a01, f32x2 a23, int lane) {
   const bool hi16 = lane & 16;
-  const float s0 = hi16 ? acc[0] : acc[2], s1 = hi16 ? acc[1] : acc[3];
-  float k0 = hi16 ? acc[2] : acc[0], k1 = hi16 ? acc[3] : acc[1];
-  k0 += __shfl_xor_sync(kFull, s0, 16);
-  k1 += __shfl_xor_sync(kFull, s1, 16);
+  const f32x2 send = hi16 ? a01 : a23;
+  f32x2 keep = hi16 ? a23 : a01;
+  const float2 sv = unpack2(send);
+  keep = add2(keep, pack2(__shfl_xor_sync(kFull, sv.x, 16), __shfl_xor_sync(kFull, sv.y, 16)));
+  const float2 kv = unpack2(keep);
   const bool hi8 = lane & 8;
-  const float s = hi8 ? k0 : k1;
-  float k = hi8 ? k1 : k0;
+  const float s = hi8 ? kv.x : kv.y;
+  float k = hi8 ? kv.y : kv.x;
   k += __shfl_xor_sync(kFull, s, 8);
   k += __shfl_xor_sync(kFull, k, 4);
   k += __shfl_xor_sync(kFull, k, 2);
@@ -135,6 +155,8 @@ __device__ __forceinline__ void stage_x(__half* buf, uint32_t bar, const __half*
   }
 }
 
+// One row quad's operands in registers: keys of q planes (4 rows each), the
+// lane's group scales (4 rows x q planes, fp16) and bias z (4 rows, fp16).
 template <int QT>
 struct Ring {
   uint4 k[QT];
@@ -142,23 +164,42 @@ struct Ring {
   uint2 z;
 };
 
+// Per-segment addressing of a lane's record fields.
+struct LaneAddr {
+  const uint8_t* seg;  // slice base in the record stream
+  uint32_t R;          // record bytes
+  uint32_t koff;       // lane's key offset in a record (plane 0)
+  uint32_t kstride;    // bytes between planes of the key block (Ls * 16)
+  uint32_t aoff;       // lane's alpha offset in a record (plane 0)
+  uint32_t zoff;       // lane's z offset in a record
+};
+
+__device__ __forceinline__ LaneAddr lane_addr(const Shape& sh, const uint8_t* data, int s, int Ls, int lay) {
+  LaneAddr a;
+  a.seg = data + slice_base(sh, s);
+  a.R = record_bytes(sh, Ls);
+  a.koff = key_off(Ls, 0, lay, 0);
+  a.kstride = (uint32_t)Ls * 16u;
+  const int k = lane_group(sh, lay);
+  a.aoff = alpha_off(sh, Ls, 0, k, 0);
+  a.zoff = z_off(sh, Ls, k, 0);
+  return a;
+}
+
 template <int QT, bool HAS_Z>
-__device__ __forceinline__ void ring_load(Ring<QT>& r, bool ok, const KParams& p, int s, int Ls, int rq, int lay,
-                                          int grp, int q) {
+__device__ __forceinline__ void ring_load(Ring<QT>& r, bool ok, const LaneAddr& la, int rq, int q) {
   if (ok) {
-    const uint8_t* bp = p.planes + plane_vec_offset(p.sh, s, Ls, rq, 0, lay);
-    const __half* ap = p.alpha + alpha_index(p.sh, rq, 0, grp, 0);
+    const uint8_t* rec = la.seg + (size_t)rq * la.R;
+    const uint8_t* kp = rec + la.koff;
+    const uint8_t* ap = rec + la.aoff;
 #pragma unroll
     for (int i = 0; i < QT; ++i) {
       if (QT <= 4 || i < q) {
-        r.k[i] = ldg_stream_u4(bp + (size_t)i * Ls * 16);
-        r.a[i] = ldg_nc_u2(ap + (size_t)i * p.sh.G * 4);
-      } else {
-        r.k[i] = make_uint4(0, 0, 0, 0);
-        r.a[i] = make_uint2(0, 0);
+        r.k[i] = ldg_stream_u4(kp + i * la.kstride);
+        r.a[i] = ldg_nc_u2(ap + 8 * i);
       }
     }
-    if (HAS_Z) r.z = ldg_nc_u2(p.offset + offset_index(p.sh, rq, grp, 0));
+    if (HAS_Z) r.z = ldg_nc_u2(rec + la.zoff);
   } else {
 #pragma unroll
     for (int i = 0; i < QT; ++i) {
@@ -169,37 +210,47 @@ __device__ __forceinline__ void ring_load(Ring<QT>& r, bool ok, const KParams& p
   }
 }
 
-// acc[r] += sum_i alpha_i[r] * (LUT partial of row r, plane i) (+ z[r] * xsum)
-template <int QT, bool HAS_Z>
-__device__ __forceinline__ void ring_compute(const Ring<QT>& r, uint32_t lc, float xsum, float acc[4], int q) {
+// (acc01, acc23) (+)= sum_i alpha_i[r] * (LUT partial of row r, plane i) (+ z[r] * xsum)
+template <int QT, bool HAS_Z, int MODE = 0>
+__device__ __forceinline__ void ring_compute(const Ring<QT>& r, uint32_t lc, float xsum, f32x2& acc01, f32x2& acc23,
+                                             int q, bool accumulate) {
 #pragma unroll
   for (int i = 0; i < QT; ++i) {
     if (QT <= 4 || i < q) {
-      const float2 a01 = h2_to_f2(r.a[i].x), a23 = h2_to_f2(r.a[i].y);
-      acc[0] = fmaf(a01.x, lut4(r.k[i].x, lc), acc[0]);
-      acc[1] = fmaf(a01.y, lut4(r.k[i].y, lc), acc[1]);
-      acc[2] = fmaf(a23.x, lut4(r.k[i].z, lc), acc[2]);
-      acc[3] = fmaf(a23.y, lut4(r.k[i].w, lc), acc[3]);
+      const f32x2 a01 = h2_to_f32x2(r.a[i].x), a23 = h2_to_f32x2(r.a[i].y);
+      const f32x2 s01 = lut4x2<MODE>(r.k[i].x, r.k[i].y, lc);
+      const f32x2 s23 = lut4x2<MODE>(r.k[i].z, r.k[i].w, lc);
+      if (i == 0 && !accumulate) {
+        acc01 = mul2(a01, s01);
+        acc23 = mul2(a23, s23);
+      } else {
+        acc01 = fma2(a01, s01, acc01);
+        acc23 = fma2(a23, s23, acc23);
+      }
     }
   }
   if (HAS_Z) {
-    const float2 z01 = h2_to_f2(r.z.x), z23 = h2_to_f2(r.z.y);
-    acc[0] = fmaf(z01.x, xsum, acc[0]);
-    acc[1] = fmaf(z01.y, xsum, acc[1]);
-    acc[2] = fmaf(z23.x, xsum, acc[2]);
-    acc[3] = fmaf(z23.y, xsum, acc[3]);
+    const f32x2 xs = pack2(xsum, xsum);
+    acc01 = fma2(h2_to_f32x2(r.z.x), xs, acc01);
+    acc23 = fma2(h2_to_f32x2(r.z.y), xs, acc23);
   }
 }
 
-__device__ __forceinline__ void store_out(const KParams& p, size_t idx, float v) {
-  if (p.yf) p.yf[idx] = v;
-  else p.y[idx] = __float2half_rn(v);
+// sum of x over the lane's 32 columns = sum_j T_{4l+j}[255]
+__device__ __forceinline__ float lane_xsum(uint32_t lut, int lane) {
+  const uint32_t k255 = 255u * 256u;
+  return (lds_f32<0>(lut + table_offset(lane, 0) + k255) + lds_f32<0>(lut + table_offset(lane, 1) + k255)) +
+         (lds_f32<0>(lut + table_offset(lane, 2) + k255) + lds_f32<0>(lut + table_offset(lane, 3) + k255));
 }
 
 // ---------------------------------------------------------------------------
 // GEMV, b = 1 (the paper's single-batch case)
+//
+// Work distribution: the S*RQ (slice, row-quad) items are split into equal
+// contiguous ranges, one per CTA (a range spans at most a few slices, so a CTA
+// builds few LUTs).  Inside a range the 16 warps take row quads round-robin.
 // ---------------------------------------------------------------------------
-template <int QT, bool HAS_Z, int PD>
+template <int QT, bool HAS_Z, int PD, int MODE = 0>
 __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31;
@@ -208,24 +259,24 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
   const int q = QT <= 4 ? QT : sh.q;
   const long long it0 = p.items * blockIdx.x / gridDim.x;
   const long long it1 = p.items * (blockIdx.x + 1) / gridDim.x;
+  unsigned long long* trace = (p.trace && tid == 0) ? p.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
+  if (trace) {
+    trace[0] = globaltimer_ns();
+    trace[7] = smid();
+  }
   if (it0 >= it1) return;
 
   const SmemMap sm = map_smem(smem);
   __half* xbuf0 = reinterpret_cast<__half*>(sm.misc_p);
   __half* xbuf1 = reinterpret_cast<__half*>(sm.misc_p + 2048);
   const uint32_t bar0 = sm.misc + 4096, bar1 = sm.misc + 4104;
-  volatile unsigned* sflag = reinterpret_cast<volatile unsigned*>(sm.misc_p + 4128);
   const uint32_t lc = (sm.lut & 0xFFFF0000u) | ((uint32_t)(4 * lane + 128) << 8) | (uint32_t)(4 * lane);
+  const int pf_steps = p.pf_steps;
 
   if (tid == 0) {
     mbar_init(bar0, 1);
     mbar_init(bar1, 1);
     fence_mbar_init();
-  }
-  __syncthreads();
-  if (warp == 0) {
-    const int s0 = (int)(it0 / sh.RQ);
-    stage_x(xbuf0, bar0, p.x, sh.n, s0 * kSliceCols, slice_lanes(sh.n, s0), 32, 1, 1, lane);
   }
   __syncthreads();
 
@@ -238,88 +289,74 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     const long long itn = it + (rq_b - rq_a);
     const int Ls = slice_lanes(sh.n, s);
     const bool lane_ok = lane < Ls;
-    const int grp = lane_ok ? (s * kSliceCols + 32 * lane) / sh.g : 0;
+    const LaneAddr la = lane_addr(sh, p.data, s, Ls, lane_ok ? lane : 0);
 
-    // 1. start streaming this segment's first row quads (independent of x)
+    // 1. the x slice of the first segment (after the PDL wait: x belongs to the
+    //    preceding kernel until it completes) is requested before anything
+    //    else, so it is not queued behind the weight stream; then an L2
+    //    prefetch of the first weight steps and the register ring
+    if (e == 0) {
+      pdl_wait();
+      if (trace) trace[5] = globaltimer_ns();
+      if (warp == 0) stage_x(xbuf0, bar0, p.x, sh.n, s * kSliceCols, Ls, 32, 1, 1, lane);
+    }
+    if (tid == 0) {
+      const int hi = min(rq_b, rq_a + pf_steps * kWarps);
+      if (hi > rq_a) bulk_prefetch_l2(la.seg + (size_t)rq_a * la.R, (uint32_t)(hi - rq_a) * la.R);
+    }
     Ring<QT> ring[PD];
 #pragma unroll
     for (int d = 0; d < PD; ++d) {
       const int rq = rq_a + warp + d * kWarps;
-      ring_load<QT, HAS_Z>(ring[d], lane_ok && rq < rq_b, p, s, Ls, rq, lane, grp, q);
+      ring_load<QT, HAS_Z>(ring[d], lane_ok && rq < rq_b, la, rq, q);
     }
+    if (e == 0) __syncthreads();  // the zero-fill of the x buffer is visible
     // 2. wait for the staged x slice and build the 128 LUTs of the slice
     __half* xb = (e & 1) ? xbuf1 : xbuf0;
     mbar_wait((e & 1) ? bar1 : bar0, (uint32_t)((e >> 1) & 1));
+    if (trace && e == 0) trace[1] = globaltimer_ns();
     {
       const int l = lane, j = warp & 3, h = warp >> 2;
       build_table_part(sm.lut + table_offset(l, j), xb + (4 * l + j) * 8, h);
     }
     __syncthreads();
+    if (trace && e == 0) trace[2] = globaltimer_ns();
     // 3. stage the next segment's x slice into the other buffer
     if (warp == 0 && itn < it1) {
       const int sn = (int)(itn / sh.RQ);
       stage_x((e & 1) ? xbuf0 : xbuf1, (e & 1) ? bar0 : bar1, p.x, sh.n, sn * kSliceCols,
               slice_lanes(sh.n, sn), 32, 1, 1, lane);
     }
-    float xsum = 0.f;
-    if (HAS_Z && lane_ok) {
-      const uint32_t k255 = 255u * 256u;
-      xsum = (lds_f32<0>(sm.lut + table_offset(lane, 0) + k255) + lds_f32<0>(sm.lut + table_offset(lane, 1) + k255)) +
-             (lds_f32<0>(sm.lut + table_offset(lane, 2) + k255) + lds_f32<0>(sm.lut + table_offset(lane, 3) + k255));
-    }
+    const float xsum = (HAS_Z && lane_ok) ? lane_xsum(sm.lut, lane) : 0.f;
+    float* part = p.partial + (size_t)s * sh.m4;
     // 4. main loop: row quads rq_a + warp + 16 t
     for (int rq0 = rq_a + warp; rq0 < rq_b; rq0 += PD * kWarps) {
 #pragma unroll
       for (int d = 0; d < PD; ++d) {
         const int rq = rq0 + d * kWarps;
         if (rq < rq_b) {
-          float acc[4] = {0.f, 0.f, 0.f, 0.f};
-          ring_compute<QT, HAS_Z>(ring[d], lc, xsum, acc, q);
-          const float v = reduce4(acc, lane);
-          if ((lane & 7) == 0) p.partial[(size_t)s * sh.m4 + 4 * rq + (lane >> 3)] = v;
+          if (tid == 0) {  // keep the L2 prefetch pf_steps steps ahead of warp 0
+            const int lo = rq + pf_steps * kWarps;
+            if (lo < rq_b)
+              bulk_prefetch_l2(la.seg + (size_t)lo * la.R, (uint32_t)(min(rq_b, lo + kWarps) - lo) * la.R);
+          }
+          f32x2 acc01, acc23;
+          ring_compute<QT, HAS_Z, MODE>(ring[d], lc, xsum, acc01, acc23, q, false);
+          const float v = reduce4(acc01, acc23, lane);
+          if ((lane & 7) == 0) part[4 * rq + (lane >> 3)] = v;
           const int rn = rq + PD * kWarps;
-          ring_load<QT, HAS_Z>(ring[d], lane_ok && rn < rq_b, p, s, Ls, rn, lane, grp, q);
+          if (MODE != 2) ring_load<QT, HAS_Z>(ring[d], lane_ok && rn < rq_b, la, rn, q);
         }
       }
     }
-    __threadfence();
-    __syncthreads();
-    // 5. arrival counters per 64-quad block; the last arrival sums the slices
-    const int blk_a = rq_a / kBlkQuads, blk_b = (rq_b - 1) / kBlkQuads;
-    for (int bb = blk_a; bb <= blk_b; bb += 32) {
-      if (warp == 0) {
-        const int blk = bb + lane;
-        unsigned done = 0;
-        if (blk <= blk_b) {
-          const int lo = max(rq_a, blk * kBlkQuads), hi = min(rq_b, (blk + 1) * kBlkQuads);
-          const unsigned cnt = (unsigned)(hi - lo);
-          const unsigned need = (unsigned)sh.S * (unsigned)(min(sh.RQ, (blk + 1) * kBlkQuads) - blk * kBlkQuads);
-          const unsigned old = atomicAdd(&p.counters[blk], cnt);
-          done = (old + cnt == need);
-        }
-        const unsigned mask = __ballot_sync(kFull, done);
-        __threadfence();
-        if (lane == 0) *sflag = mask;
-      }
-      __syncthreads();
-      unsigned mask = *sflag;
-      while (mask) {
-        const int blk = bb + __ffs(mask) - 1;
-        mask &= mask - 1;
-        const int row = blk * kBlkQuads * 4 + tid;
-        if (tid < kBlkQuads * 4 && row < sh.m) {
-          float v = 0.f;
-          const float* pp = p.partial + row;
-          for (int ss = 0; ss < sh.S; ++ss) v += __ldcg(pp + (size_t)ss * sh.m4);
-          store_out(p, (size_t)row, v);
-        }
-        if (tid == 0) p.counters[blk] = 0u;
-      }
-      __syncthreads();
-    }
+    if (trace && e == 0) trace[3] = globaltimer_ns();  // warp 0's loop end
+    __syncthreads();  // the LUT and x buffer are reused by the next segment
+    if (trace) trace[e == 0 ? 4 : 6] = globaltimer_ns();  // all warps done
     it = itn;
     ++e;
   }
+  if (trace) trace[7] |= (unsigned long long)e << 32;  // segments processed
+  pdl_launch_dependents();  // the reduction kernel may now be scheduled
 }
 
 // ---------------------------------------------------------------------------
@@ -337,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemm_batched_kernel(const KPa
   const int q = QT <= 4 ? QT : sh.q;
   const int bl = p.bl, B = 1 << bl, P = 32 >> bl, b = p.b;
   const int beta = lane & (B - 1), pp = lane >> bl;
-  const int rbq = kWarps * kQPW;                      // row quads per work item
+  const int rbq = kWarps * kQPW;  // row quads per work item
   const int NRB = (sh.RQ + rbq - 1) / rbq;
   const long long it0 = p.items * blockIdx.x / gridDim.x;
   const long long it1 = p.items * (blockIdx.x + 1) / gridDim.x;
@@ -347,15 +384,15 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemm_batched_kernel(const KPa
   __half* xbuf0 = reinterpret_cast<__half*>(sm.misc_p);
   __half* xbuf1 = reinterpret_cast<__half*>(sm.misc_p + 2048);
   const uint32_t bar0 = sm.misc + 4096, bar1 = sm.misc + 4104;
-  volatile unsigned* sflag = reinterpret_cast<volatile unsigned*>(sm.misc_p + 4128);
   const uint32_t lc = (sm.lut & 0xFFFF0000u) | ((uint32_t)(4 * lane + 128) << 8) | (uint32_t)(4 * lane);
 
-  if (tid == 0) {
-    mbar_init(bar0, 1);
-    mbar_init(bar1, 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
+  // the records of item itx (one contiguous range) into L2
+  auto prefetch_item = [&](long long itx) {
+    const int s = (int)(itx / NRB), rb = (int)(itx % NRB);
+    const int Ls = slice_lanes(sh.n, s);
+    const int lo = rb * rbq, hi = min(sh.RQ, lo + rbq);
+    bulk_prefetch_l2(p.data + record_offset(sh, s, Ls, lo), (uint32_t)(hi - lo) * record_bytes(sh, Ls));
+  };
   // staging of sub-slice (s, k): P lanes starting at layout lane k*P
   auto stage = [&](int ebuf, long long itx, int k) {
     const int s = (int)(itx / NRB);
@@ -364,6 +401,15 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemm_batched_kernel(const KPa
     stage_x((ebuf & 1) ? xbuf1 : xbuf0, (ebuf & 1) ? bar1 : bar0, p.x, sh.n, s * kSliceCols + 32 * k * P, nl, P,
             min(b, B), B, lane);
   };
+
+  if (tid == 0) {
+    mbar_init(bar0, 1);
+    mbar_init(bar1, 1);
+    fence_mbar_init();
+    prefetch_item(it0);
+  }
+  pdl_wait();  // x and the workspace belong to the preceding kernel until it completes
+  __syncthreads();
   if (warp == 0) stage(0, it0, 0);
   __syncthreads();
 
@@ -373,19 +419,17 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemm_batched_kernel(const KPa
     const int rb = (int)(it % NRB);
     const int Ls = slice_lanes(sh.n, s);
     const int nsub = (Ls + P - 1) / P;
-    const int rq_w = rb * rbq + warp * kQPW;           // this warp's first quad
-    float acc[kQPW][4];
-#pragma unroll
-    for (int t = 0; t < kQPW; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
+    const int rq_w = rb * rbq + warp * kQPW;  // this warp's first quad
+    if (tid == 0 && it + 1 < it1) prefetch_item(it + 1);
+    f32x2 acc01[kQPW], acc23[kQPW];
 
     for (int k = 0; k < nsub; ++k, ++e) {
       const int lay = k * P + pp;
       const bool lane_ok = lay < Ls;
-      const int grp = lane_ok ? (s * kSliceCols + 32 * lay) / sh.g : 0;
+      const LaneAddr la = lane_addr(sh, p.data, s, Ls, lane_ok ? lay : 0);
       Ring<QT> ring[PD];
 #pragma unroll
-      for (int d = 0; d < PD; ++d)
-        ring_load<QT, HAS_Z>(ring[d], lane_ok && rq_w + d < sh.RQ, p, s, Ls, rq_w + d, lay, grp, q);
+      for (int d = 0; d < PD; ++d) ring_load<QT, HAS_Z>(ring[d], lane_ok && rq_w + d < sh.RQ, la, rq_w + d, q);
       __half* xb = (e & 1) ? xbuf1 : xbuf0;
       mbar_wait((e & 1) ? bar1 : bar0, (uint32_t)((e >> 1) & 1));
       {
@@ -398,62 +442,76 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemm_batched_kernel(const KPa
         if (k + 1 < nsub) stage(e + 1, it, k + 1);
         else if (it + 1 < it1) stage(e + 1, it + 1, 0);
       }
-      float xsum = 0.f;
-      if (HAS_Z && lane_ok) {
-        const uint32_t k255 = 255u * 256u;
-        xsum = (lds_f32<0>(sm.lut + table_offset(lane, 0) + k255) + lds_f32<0>(sm.lut + table_offset(lane, 1) + k255)) +
-               (lds_f32<0>(sm.lut + table_offset(lane, 2) + k255) + lds_f32<0>(sm.lut + table_offset(lane, 3) + k255));
-      }
+      const float xsum = (HAS_Z && lane_ok) ? lane_xsum(sm.lut, lane) : 0.f;
 #pragma unroll
       for (int t = 0; t < kQPW; ++t) {
         const int d = t % PD;
-        ring_compute<QT, HAS_Z>(ring[d], lc, xsum, acc[t], q);
-        if (t + PD < kQPW)
-          ring_load<QT, HAS_Z>(ring[d], lane_ok && rq_w + t + PD < sh.RQ, p, s, Ls, rq_w + t + PD, lay, grp, q);
+        ring_compute<QT, HAS_Z>(ring[d], lc, xsum, acc01[t], acc23[t], q, k > 0);
+        if (t + PD < kQPW) ring_load<QT, HAS_Z>(ring[d], lane_ok && rq_w + t + PD < sh.RQ, la, rq_w + t + PD, q);
       }
       __syncthreads();  // LUT is rebuilt next
     }
     // reduce over the P layout lanes that share a batch row (lane bits >= bl)
 #pragma unroll
     for (int t = 0; t < kQPW; ++t) {
+      float2 v01 = unpack2(acc01[t]), v23 = unpack2(acc23[t]);
+      for (int off = 16; off >= B; off >>= 1) {
+        v01.x += __shfl_xor_sync(kFull, v01.x, off);
+        v01.y += __shfl_xor_sync(kFull, v01.y, off);
+        v23.x += __shfl_xor_sync(kFull, v23.x, off);
+        v23.y += __shfl_xor_sync(kFull, v23.y, off);
+      }
+      const int rq = rq_w + t;
+      if (pp == 0 && beta < b && rq < sh.RQ) {
+        float* dst = p.partial + ((size_t)s * b + beta) * sh.m4 + 4 * rq;
+        *reinterpret_cast<float4*>(dst) = make_float4(v01.x, v01.y, v23.x, v23.y);
+      }
+    }
+  }
+  pdl_launch_dependents();
+}
+
+// ---------------------------------------------------------------------------
+// Cross-slice reduction: Y[beta][r] = sum_{s=0}^{S-1} partial[s][beta][r] in
+// slice order (deterministic, R11), then fp16 round-to-nearest-even (or fp32).
+// One thread per (beta, row quad); launched with PDL after the LUT kernel.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) lut_reduce_kernel(const float* __restrict__ partial, int S, int b, int m,
+                                                         int m4, __half* __restrict__ y, float* __restrict__ yf,
+                                                         unsigned* __restrict__ counters) {
+  pdl_launch_dependents();  // the next product may start streaming its weights
+  pdl_wait();               // partials are complete and visible
+  if (blockIdx.x == 0)
+    for (int t = threadIdx.x; t < S; t += blockDim.x) counters[t] = 0u;  // chunk counters for the next launch
+  const int RQ = m4 / 4;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= b * RQ) return;
+  const int beta = idx / RQ, rq = idx % RQ;
+  const float4* src = reinterpret_cast<const float4*>(partial + (size_t)beta * m4) + rq;
+  const size_t stride = (size_t)b * RQ;  // float4 units between slices
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int s0 = 0; s0 < S; s0 += 8) {
+    float4 v[8];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        float v = acc[t][r];
-        for (int off = 16; off >= B; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
-        acc[t][r] = v;
-      }
-    }
-    if (pp == 0 && beta < b) {
+    for (int k = 0; k < 8; ++k) v[k] = (s0 + k < S) ? __ldcg(src + (size_t)(s0 + k) * stride) : make_float4(0, 0, 0, 0);
 #pragma unroll
-      for (int t = 0; t < kQPW; ++t) {
-        const int rq = rq_w + t;
-        if (rq < sh.RQ) {
-          float* dst = p.partial + ((size_t)s * b + beta) * sh.m4 + 4 * rq;
-          *reinterpret_cast<float4*>(dst) = make_float4(acc[t][0], acc[t][1], acc[t][2], acc[t][3]);
-        }
+    for (int k = 0; k < 8; ++k)
+      if (s0 + k < S) {
+        acc.x += v[k].x;
+        acc.y += v[k].y;
+        acc.z += v[k].z;
+        acc.w += v[k].w;
       }
+  }
+  const float r[4] = {acc.x, acc.y, acc.z, acc.w};
+  const int row0 = 4 * rq;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (row0 + k < m) {
+      const size_t o = (size_t)beta * m + row0 + k;
+      if (yf) yf[o] = r[k];
+      else y[o] = __float2half_rn(r[k]);
     }
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) {
-      const unsigned old = atomicAdd(&p.counters[rb], 1u);
-      __threadfence();
-      *sflag = (old + 1 == (unsigned)sh.S) ? 1u : 0u;
-    }
-    __syncthreads();
-    if (*sflag) {
-      const int row0 = rb * rbq * 4;
-      const int nrows = min(sh.m, row0 + rbq * 4) - row0;
-      for (int idx = tid; idx < nrows * b; idx += kThreads) {
-        const int bt = idx / nrows, row = row0 + idx % nrows;
-        float v = 0.f;
-        const float* pp2 = p.partial + (size_t)bt * sh.m4 + row;
-        for (int ss = 0; ss < sh.S; ++ss) v += __ldcg(pp2 + (size_t)ss * b * sh.m4);
-        store_out(p, (size_t)bt * sh.m + row, v);
-      }
-      if (tid == 0) p.counters[rb] = 0u;
-    }
-    __syncthreads();
   }
 }
 
@@ -474,17 +532,58 @@ static int num_sms() {
   return g_num_sms[dev];
 }
 
+static cudaLaunchAttribute g_pdl_attr = [] {
+  cudaLaunchAttribute a;
+  a.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a.val.programmaticStreamSerializationAllowed = 1;
+  return a;
+}();
+
 template <typename K>
 static cudaError_t launch(K kernel, int grid, const KParams& p, cudaStream_t st) {
   cudaError_t err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
   if (err != cudaSuccess) return err;
-  kernel<<<grid, kThreads, kSmemBytes, st>>>(p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = st;
+  cfg.attrs = &g_pdl_attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, p);
+}
+
+static cudaError_t launch_reduce(const KParams& p, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {  // keep the max-shared-memory carveout: no L1/smem reconfiguration between the two kernels
+    cudaFuncSetAttribute(lut_reduce_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    attr_set = true;
+  }
+  const int threads = 256;
+  const int total = p.b * p.sh.RQ;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((total + threads - 1) / threads);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cfg.attrs = &g_pdl_attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, lut_reduce_kernel, (const float*)p.partial, p.sh.S, p.b, p.sh.m, p.sh.m4, p.y,
+                            p.yf, p.counters);
 }
 
 template <int QT, bool HAS_Z>
 static cudaError_t launch_gemv_t(const KParams& p, int grid, cudaStream_t st) {
   constexpr int PD = QT <= 1 ? 6 : (QT <= 2 ? 4 : (QT <= 4 ? 3 : 1));
+  if (QT == 3 && !HAS_Z && p.xmode >= 10) {  // measurement variants (LUTGEMM_XMODE)
+    switch (p.xmode) {
+      case 10: return launch(lut_gemv_kernel<QT, HAS_Z, 2, 0>, grid, p, st);
+      case 11: return launch(lut_gemv_kernel<QT, HAS_Z, 3, 1>, grid, p, st);
+      case 12: return launch(lut_gemv_kernel<QT, HAS_Z, 3, 2>, grid, p, st);
+      case 14: return launch(lut_gemv_kernel<QT, HAS_Z, 4, 0>, grid, p, st);
+      default: break;
+    }
+  }
   return launch(lut_gemv_kernel<QT, HAS_Z, PD>, grid, p, st);
 }
 
@@ -505,21 +604,41 @@ static cudaError_t dispatch_q(const KParams& p, int grid, cudaStream_t st, bool 
   }
 }
 
-size_t counters_bytes(const Shape& sh) {
-  const size_t n = (size_t)(sh.RQ + 15) / 16;
-  return (n * 4 + 255) / 256 * 256;
-}
+static size_t counters_bytes(const Shape& sh) { return ((size_t)sh.S * 4u + 255) / 256 * 256; }
 
 size_t workspace_bytes(const Shape& sh, int b) {
-  return counters_bytes(sh) + (size_t)sh.S * (size_t)b * (size_t)sh.m4 * 4u;
+  return counters_bytes(sh) + ((size_t)sh.S * (size_t)b * (size_t)sh.m4 * 4u + 255) / 256 * 256;
 }
 
-cudaError_t run_product(const Shape& sh, const void* planes, const void* alpha, const void* offset,
-                        const uint16_t* x, int b, uint16_t* y, float* yf, void* ws, cudaStream_t st) {
+static int g_pf_steps = -1;
+static unsigned long long* g_trace = nullptr;
+static bool g_trace_on = false;
+constexpr int kTraceMaxCtas = 1024;
+
+void trace_enable(int on) {
+  g_trace_on = on != 0;
+  if (g_trace_on && !g_trace) {
+    cudaMalloc(&g_trace, sizeof(unsigned long long) * kTraceSlots * kTraceMaxCtas);
+    cudaMemset(g_trace, 0, sizeof(unsigned long long) * kTraceSlots * kTraceMaxCtas);
+  }
+}
+
+size_t trace_read(unsigned long long* host, size_t n) {
+  if (!g_trace || !host) return 0;
+  const size_t cap = (size_t)kTraceSlots * kTraceMaxCtas;
+  if (n > cap) n = cap;
+  cudaMemcpy(host, g_trace, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  return n;
+}
+
+cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, int b, uint16_t* y, float* yf,
+                        void* ws, cudaStream_t st) {
+  if (g_pf_steps < 0) {
+    const char* env = getenv("LUTGEMM_PF_STEPS");  // tuning knob (default kPfSteps)
+    g_pf_steps = env ? atoi(env) : kPfSteps;
+  }
   KParams p;
-  p.planes = static_cast<const uint8_t*>(planes);
-  p.alpha = static_cast<const __half*>(alpha);
-  p.offset = static_cast<const __half*>(offset);
+  p.data = static_cast<const uint8_t*>(data);
   p.x = reinterpret_cast<const __half*>(x);
   p.y = reinterpret_cast<__half*>(y);
   p.yf = yf;
@@ -530,6 +649,12 @@ cudaError_t run_product(const Shape& sh, const void* planes, const void* alpha, 
   int bl = 0;
   while ((1 << bl) < b) ++bl;
   p.bl = bl;
+  p.pf_steps = g_pf_steps;
+  {
+    const char* env = getenv("LUTGEMM_XMODE");  // experiment knob
+    p.xmode = env ? atoi(env) : 0;
+  }
+  p.trace = g_trace_on ? g_trace : nullptr;
   const bool batched = b > 1;
   if (!batched) {
     p.items = (long long)sh.S * sh.RQ;
@@ -538,7 +663,9 @@ cudaError_t run_product(const Shape& sh, const void* planes, const void* alpha, 
     p.items = (long long)sh.S * ((sh.RQ + rbq - 1) / rbq);
   }
   const int grid = (int)std::min<long long>((long long)num_sms(), p.items);
-  return offset ? dispatch_q<true>(p, grid, st, batched) : dispatch_q<false>(p, grid, st, batched);
+  cudaError_t e = sh.has_z ? dispatch_q<true>(p, grid, st, batched) : dispatch_q<false>(p, grid, st, batched);
+  if (e != cudaSuccess) return e;
+  return launch_reduce(p, st);
 }
 
 }  // namespace lg

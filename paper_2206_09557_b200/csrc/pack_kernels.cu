@@ -1,6 +1,7 @@
 // pack_kernels.cu -- offline repacking into the kernel-native layout (layout.cuh).
 //
-// BCQ source: canonical planes/alpha/offset are permuted, bit for bit.
+// BCQ source: canonical planes/alpha/offset are permuted into the record
+// stream of layout.cuh, bit for bit.
 // UNIFORM source: App. C -- plane i bit = bit i of the code
 // (b_i = 2 b_hat_i - 1), alpha_i = 2^(i-1) s (exact power-of-two
 // scaling of an fp16 s), z = sum_i alpha_i + z_hat summed in fp64 and rounded
@@ -24,7 +25,7 @@ inline int blocks_for(size_t total) {
   return (int)(b > 65535u * 16u ? 65535u * 16u : (b ? b : 1));
 }
 
-__global__ void pack_planes_kernel(const uint32_t* __restrict__ src, uint8_t* __restrict__ dst, Shape sh) {
+__global__ void pack_keys_kernel(const uint32_t* __restrict__ src, uint8_t* __restrict__ dst, Shape sh) {
   const int nw = sh.n / 32;
   const size_t total = (size_t)sh.q * sh.m4 * nw;
   for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
@@ -34,11 +35,11 @@ __global__ void pack_planes_kernel(const uint32_t* __restrict__ src, uint8_t* __
     const uint32_t v = r < sh.m ? src[((size_t)i * sh.m + r) * nw + w] : 0u;
     const int s = w / kLanesPerSlice, p = w % kLanesPerSlice;
     const int Ls = slice_lanes(sh.n, s);
-    *reinterpret_cast<uint32_t*>(dst + plane_vec_offset(sh, s, Ls, r / 4, i, p) + (r % 4) * 4) = v;
+    *reinterpret_cast<uint32_t*>(dst + record_offset(sh, s, Ls, r / 4) + key_off(Ls, i, p, r % 4)) = v;
   }
 }
 
-__global__ void unpack_planes_kernel(const uint8_t* __restrict__ src, uint32_t* __restrict__ dst, Shape sh) {
+__global__ void unpack_keys_kernel(const uint8_t* __restrict__ src, uint32_t* __restrict__ dst, Shape sh) {
   const int nw = sh.n / 32;
   const size_t total = (size_t)sh.q * sh.m * nw;
   for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
@@ -47,56 +48,66 @@ __global__ void unpack_planes_kernel(const uint8_t* __restrict__ src, uint32_t* 
     const int i = (int)(idx / ((size_t)nw * sh.m));
     const int s = w / kLanesPerSlice, p = w % kLanesPerSlice;
     const int Ls = slice_lanes(sh.n, s);
-    dst[idx] = *reinterpret_cast<const uint32_t*>(src + plane_vec_offset(sh, s, Ls, r / 4, i, p) + (r % 4) * 4);
+    dst[idx] = *reinterpret_cast<const uint32_t*>(src + record_offset(sh, s, Ls, r / 4) + key_off(Ls, i, p, r % 4));
   }
 }
 
-// alpha canonical [m][G][q] <-> native [RQ][q][G][4]
-__global__ void pack_alpha_kernel(const uint16_t* __restrict__ src, uint16_t* __restrict__ dst, Shape sh) {
-  const size_t total = alpha_elems(sh);
+// scales: one thread per (slice, row quad, slice-local group k); writes alpha
+// for all q planes and z (canonical alpha [m][G][q], z [m][G]).
+__global__ void pack_scales_kernel(const uint16_t* __restrict__ alpha, const uint16_t* __restrict__ offset,
+                                   uint8_t* __restrict__ dst, Shape sh) {
+  const int gmax = slice_groups(sh, kLanesPerSlice);
+  const size_t total = (size_t)sh.S * sh.RQ * gmax;
   for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
-    const int r4 = (int)(idx % 4);
-    const int grp = (int)((idx / 4) % sh.G);
-    const int i = (int)((idx / (4 * (size_t)sh.G)) % sh.q);
-    const int rq = (int)(idx / (4 * (size_t)sh.G * sh.q));
-    const int r = 4 * rq + r4;
-    dst[idx] = r < sh.m ? src[((size_t)r * sh.G + grp) * sh.q + i] : (uint16_t)0;
+    const int k = (int)(idx % gmax);
+    const int rq = (int)((idx / gmax) % sh.RQ);
+    const int s = (int)(idx / ((size_t)gmax * sh.RQ));
+    const int Ls = slice_lanes(sh.n, s);
+    if (k >= slice_groups(sh, Ls)) continue;
+    const int grp = global_group(sh, s, k);
+    uint8_t* rec = dst + record_offset(sh, s, Ls, rq);
+    for (int r4 = 0; r4 < 4; ++r4) {
+      const int r = 4 * rq + r4;
+      for (int i = 0; i < sh.q; ++i)
+        *reinterpret_cast<uint16_t*>(rec + alpha_off(sh, Ls, i, k, r4)) =
+            r < sh.m ? alpha[((size_t)r * sh.G + grp) * sh.q + i] : (uint16_t)0;
+      if (sh.has_z)
+        *reinterpret_cast<uint16_t*>(rec + z_off(sh, Ls, k, r4)) =
+            (r < sh.m && offset) ? offset[(size_t)r * sh.G + grp] : (uint16_t)0;
+    }
   }
 }
 
-__global__ void unpack_alpha_kernel(const uint16_t* __restrict__ src, uint16_t* __restrict__ dst, Shape sh) {
-  const size_t total = (size_t)sh.m * sh.G * sh.q;
-  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
-    const int i = (int)(idx % sh.q);
-    const int grp = (int)((idx / sh.q) % sh.G);
-    const int r = (int)(idx / ((size_t)sh.q * sh.G));
-    dst[idx] = src[alpha_index(sh, r / 4, i, grp, r % 4)];
+// first slice that stores group grp, and the group's slice-local index
+__device__ inline void home_of_group(const Shape& sh, int grp, int* s, int* k) {
+  if (sh.g <= kSliceCols) {
+    *s = grp / (kSliceCols / sh.g);
+    *k = grp % (kSliceCols / sh.g);
+  } else {
+    *s = (int)(((long long)grp * sh.g) / kSliceCols);
+    *k = 0;
   }
 }
 
-// offset canonical [m][G] <-> native [RQ][G][4]
-__global__ void pack_offset_kernel(const uint16_t* __restrict__ src, uint16_t* __restrict__ dst, Shape sh) {
-  const size_t total = offset_elems(sh);
-  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
-    const int r4 = (int)(idx % 4);
-    const int grp = (int)((idx / 4) % sh.G);
-    const int rq = (int)(idx / (4 * (size_t)sh.G));
-    const int r = 4 * rq + r4;
-    dst[idx] = r < sh.m ? src[(size_t)r * sh.G + grp] : (uint16_t)0;
-  }
-}
-
-__global__ void unpack_offset_kernel(const uint16_t* __restrict__ src, uint16_t* __restrict__ dst, Shape sh) {
+__global__ void unpack_scales_kernel(const uint8_t* __restrict__ src, uint16_t* __restrict__ alpha,
+                                     uint16_t* __restrict__ offset, Shape sh) {
   const size_t total = (size_t)sh.m * sh.G;
   for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
     const int grp = (int)(idx % sh.G);
     const int r = (int)(idx / sh.G);
-    dst[idx] = src[offset_index(sh, r / 4, grp, r % 4)];
+    int s, k;
+    home_of_group(sh, grp, &s, &k);
+    const int Ls = slice_lanes(sh.n, s);
+    const uint8_t* rec = src + record_offset(sh, s, Ls, r / 4);
+    if (alpha)
+      for (int i = 0; i < sh.q; ++i)
+        alpha[idx * sh.q + i] = *reinterpret_cast<const uint16_t*>(rec + alpha_off(sh, Ls, i, k, r % 4));
+    if (offset && sh.has_z) offset[idx] = *reinterpret_cast<const uint16_t*>(rec + z_off(sh, Ls, k, r % 4));
   }
 }
 
-// uniform codes [m][n] -> native planes: plane i word = bit i of 32 codes
-__global__ void pack_uniform_planes_kernel(const uint8_t* __restrict__ codes, uint8_t* __restrict__ dst, Shape sh) {
+// uniform codes [m][n] -> keys: plane i word = bit i of 32 codes (b_hat_i, App. C)
+__global__ void pack_uniform_keys_kernel(const uint8_t* __restrict__ codes, uint8_t* __restrict__ dst, Shape sh) {
   const int nw = sh.n / 32;
   const size_t total = (size_t)sh.m4 * nw;
   for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
@@ -112,68 +123,75 @@ __global__ void pack_uniform_planes_kernel(const uint8_t* __restrict__ codes, ui
     }
     const int s = w / kLanesPerSlice, p = w % kLanesPerSlice;
     const int Ls = slice_lanes(sh.n, s);
-    for (int i = 0; i < sh.q; ++i)
-      *reinterpret_cast<uint32_t*>(dst + plane_vec_offset(sh, s, Ls, r / 4, i, p) + (r % 4) * 4) = words[i];
+    uint8_t* rec = dst + record_offset(sh, s, Ls, r / 4);
+    for (int i = 0; i < sh.q; ++i) *reinterpret_cast<uint32_t*>(rec + key_off(Ls, i, p, r % 4)) = words[i];
   }
 }
 
-// alpha_i = 2^(i-1) s ; z = sum_i alpha_i + z_hat  (App. C Eq. 8)
+// alpha_i = 2^(i-1) s ; z = sum_i alpha_i + z_hat  (App. C Eq. 8), per (slice, rq, k)
 __global__ void pack_uniform_scales_kernel(const uint16_t* __restrict__ scale, const uint16_t* __restrict__ zero,
-                                           uint16_t* __restrict__ alpha, uint16_t* __restrict__ offset, Shape sh) {
-  const size_t total = offset_elems(sh);  // one thread per (rq, grp, r4)
+                                           uint8_t* __restrict__ dst, Shape sh) {
+  const int gmax = slice_groups(sh, kLanesPerSlice);
+  const size_t total = (size_t)sh.S * sh.RQ * gmax;
   for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
-    const int r4 = (int)(idx % 4);
-    const int grp = (int)((idx / 4) % sh.G);
-    const int rq = (int)(idx / (4 * (size_t)sh.G));
-    const int r = 4 * rq + r4;
-    double s = 0.0, zh = 0.0;
-    if (r < sh.m) {
-      s = (double)__half2float(__ushort_as_half(scale[(size_t)r * sh.G + grp]));
-      zh = (double)__half2float(__ushort_as_half(zero[(size_t)r * sh.G + grp]));
+    const int k = (int)(idx % gmax);
+    const int rq = (int)((idx / gmax) % sh.RQ);
+    const int s = (int)(idx / ((size_t)gmax * sh.RQ));
+    const int Ls = slice_lanes(sh.n, s);
+    if (k >= slice_groups(sh, Ls)) continue;
+    const int grp = global_group(sh, s, k);
+    uint8_t* rec = dst + record_offset(sh, s, Ls, rq);
+    for (int r4 = 0; r4 < 4; ++r4) {
+      const int r = 4 * rq + r4;
+      double sv = 0.0, zh = 0.0;
+      if (r < sh.m) {
+        sv = (double)__half2float(__ushort_as_half(scale[(size_t)r * sh.G + grp]));
+        zh = (double)__half2float(__ushort_as_half(zero[(size_t)r * sh.G + grp]));
+      }
+      double sum_alpha = 0.0;
+      for (int i = 0; i < sh.q; ++i) {
+        const double a = ldexp(sv, i - 1);
+        sum_alpha += a;
+        *reinterpret_cast<uint16_t*>(rec + alpha_off(sh, Ls, i, k, r4)) = __half_as_ushort(__double2half(a));
+      }
+      *reinterpret_cast<uint16_t*>(rec + z_off(sh, Ls, k, r4)) =
+          __half_as_ushort(__double2half(r < sh.m ? sum_alpha + zh : 0.0));
     }
-    double sum_alpha = 0.0;
-    for (int i = 0; i < sh.q; ++i) {
-      const double a = ldexp(s, i - 1);
-      sum_alpha += a;
-      alpha[alpha_index(sh, rq, i, grp, r4)] = __half_as_ushort(__double2half(a));
-    }
-    offset[offset_index(sh, rq, grp, r4)] = __half_as_ushort(__double2half(r < sh.m ? sum_alpha + zh : 0.0));
   }
 }
 
 }  // namespace
 
 cudaError_t run_pack_bcq(const Shape& sh, const uint32_t* planes, const uint16_t* alpha, const uint16_t* offset,
-                         void* dplanes, void* dalpha, void* doffset, cudaStream_t st) {
-  pack_planes_kernel<<<blocks_for((size_t)sh.q * sh.m4 * (sh.n / 32)), kPackThreads, 0, st>>>(
-      planes, static_cast<uint8_t*>(dplanes), sh);
-  pack_alpha_kernel<<<blocks_for(alpha_elems(sh)), kPackThreads, 0, st>>>(alpha, static_cast<uint16_t*>(dalpha), sh);
-  if (offset && doffset)
-    pack_offset_kernel<<<blocks_for(offset_elems(sh)), kPackThreads, 0, st>>>(offset, static_cast<uint16_t*>(doffset),
-                                                                             sh);
+                         void* dst, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(dst, 0, packed_bytes(sh), st);
+  if (e != cudaSuccess) return e;
+  pack_keys_kernel<<<blocks_for((size_t)sh.q * sh.m4 * (sh.n / 32)), kPackThreads, 0, st>>>(
+      planes, static_cast<uint8_t*>(dst), sh);
+  pack_scales_kernel<<<blocks_for((size_t)sh.S * sh.RQ * slice_groups(sh, kLanesPerSlice)), kPackThreads, 0, st>>>(
+      alpha, offset, static_cast<uint8_t*>(dst), sh);
   return cudaGetLastError();
 }
 
 cudaError_t run_pack_uniform(const Shape& sh, const uint8_t* codes, const uint16_t* scale, const uint16_t* zero,
-                             void* dplanes, void* dalpha, void* doffset, cudaStream_t st) {
-  pack_uniform_planes_kernel<<<blocks_for((size_t)sh.m4 * (sh.n / 32)), kPackThreads, 0, st>>>(
-      codes, static_cast<uint8_t*>(dplanes), sh);
-  pack_uniform_scales_kernel<<<blocks_for(offset_elems(sh)), kPackThreads, 0, st>>>(
-      scale, zero, static_cast<uint16_t*>(dalpha), static_cast<uint16_t*>(doffset), sh);
+                             void* dst, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(dst, 0, packed_bytes(sh), st);
+  if (e != cudaSuccess) return e;
+  pack_uniform_keys_kernel<<<blocks_for((size_t)sh.m4 * (sh.n / 32)), kPackThreads, 0, st>>>(
+      codes, static_cast<uint8_t*>(dst), sh);
+  pack_uniform_scales_kernel<<<blocks_for((size_t)sh.S * sh.RQ * slice_groups(sh, kLanesPerSlice)), kPackThreads, 0,
+                               st>>>(scale, zero, static_cast<uint8_t*>(dst), sh);
   return cudaGetLastError();
 }
 
-cudaError_t run_unpack(const Shape& sh, const void* dplanes, const void* dalpha, const void* doffset,
-                       uint32_t* planes, uint16_t* alpha, uint16_t* offset, cudaStream_t st) {
+cudaError_t run_unpack(const Shape& sh, const void* src, uint32_t* planes, uint16_t* alpha, uint16_t* offset,
+                       cudaStream_t st) {
   if (planes)
-    unpack_planes_kernel<<<blocks_for((size_t)sh.q * sh.m * (sh.n / 32)), kPackThreads, 0, st>>>(
-        static_cast<const uint8_t*>(dplanes), planes, sh);
-  if (alpha)
-    unpack_alpha_kernel<<<blocks_for((size_t)sh.m * sh.G * sh.q), kPackThreads, 0, st>>>(
-        static_cast<const uint16_t*>(dalpha), alpha, sh);
-  if (offset && doffset)
-    unpack_offset_kernel<<<blocks_for((size_t)sh.m * sh.G), kPackThreads, 0, st>>>(
-        static_cast<const uint16_t*>(doffset), offset, sh);
+    unpack_keys_kernel<<<blocks_for((size_t)sh.q * sh.m * (sh.n / 32)), kPackThreads, 0, st>>>(
+        static_cast<const uint8_t*>(src), planes, sh);
+  if (alpha || offset)
+    unpack_scales_kernel<<<blocks_for((size_t)sh.m * sh.G), kPackThreads, 0, st>>>(static_cast<const uint8_t*>(src),
+                                                                                  alpha, offset, sh);
   return cudaGetLastError();
 }
 

@@ -30,8 +30,7 @@ class LutgemmError(RuntimeError):
 
 class lutgemm_weight(ctypes.Structure):
     _fields_ = [("m", ctypes.c_int32), ("n", ctypes.c_int32), ("q", ctypes.c_int32), ("g", ctypes.c_int32),
-                ("has_offset", ctypes.c_int32), ("reserved", ctypes.c_int32),
-                ("planes", ctypes.c_void_p), ("alpha", ctypes.c_void_p), ("offset", ctypes.c_void_p)]
+                ("has_offset", ctypes.c_int32), ("reserved", ctypes.c_int32), ("data", ctypes.c_void_p)]
 
 
 class lutgemm_pack_src(ctypes.Structure):
@@ -48,7 +47,7 @@ _I = ctypes.c_int
 SIGNATURES = [
     ("lutgemm_abi_version", _I, []),
     ("lutgemm_last_error", ctypes.c_char_p, []),
-    ("lutgemm_packed_bytes", _I, [_I, _I, _I, _I, _I, ctypes.POINTER(_SZ), ctypes.POINTER(_SZ), ctypes.POINTER(_SZ)]),
+    ("lutgemm_packed_bytes", _I, [_I, _I, _I, _I, _I, ctypes.POINTER(_SZ)]),
     ("lutgemm_pack_bcq", _I, [ctypes.POINTER(lutgemm_pack_src), ctypes.POINTER(lutgemm_weight), _P]),
     ("lutgemm_unpack_bcq", _I, [ctypes.POINTER(lutgemm_weight), _P, _P, _P, _P]),
     ("lutgemm_workspace_bytes", _SZ, [_I, _I, _I]),
@@ -58,6 +57,8 @@ SIGNATURES = [
     ("lutgemm_gemm_batched_f32", _I, [ctypes.POINTER(lutgemm_weight), _P, _I, _P, _P, _SZ, _P]),
     ("lutgemm_host_workspace_bytes", _SZ, [_I, _I, _I]),
     ("lutgemm_gemm_host", _I, [ctypes.POINTER(lutgemm_weight), _P, _I, _P, _P, _SZ, _P]),
+    ("lutgemm_trace_enable", _I, [_I]),
+    ("lutgemm_trace_read", _SZ, [ctypes.POINTER(ctypes.c_uint64), _SZ]),
     ("lutgemm_tp_unique_id", _I, [_P]),
     ("lutgemm_tp_init", _I, [_I, _I, _P, ctypes.POINTER(_P)]),
     ("lutgemm_tp_workspace_bytes", _SZ, [_P, _I, _I, _I, _I]),
@@ -97,40 +98,33 @@ def _stream(stream=None) -> int:
     return s.cuda_stream
 
 
-def lutgemm_packed_bytes(m: int, n: int, q: int, g: int, has_offset: bool) -> tuple[int, int, int]:
-    a, b, c = _SZ(), _SZ(), _SZ()
-    _check("lutgemm_packed_bytes",
-           lib.lutgemm_packed_bytes(m, n, q, g, int(has_offset), ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
-    return a.value, b.value, c.value
+def lutgemm_packed_bytes(m: int, n: int, q: int, g: int, has_offset: bool) -> int:
+    a = _SZ()
+    _check("lutgemm_packed_bytes", lib.lutgemm_packed_bytes(m, n, q, g, int(has_offset), ctypes.byref(a)))
+    return a.value
 
 
 @dataclass
 class PackedBCQ:
-    """A packed weight resident on the device (kernel-native layout); the
-    three torch tensors own the memory, ``struct`` is the C view of them."""
+    """A packed weight resident on the device (kernel-native record stream);
+    the torch tensor ``data`` owns the memory, ``struct`` is its C view."""
     m: int
     n: int
     q: int
     g: int
     has_offset: bool
-    planes: torch.Tensor
-    alpha: torch.Tensor
-    offset: torch.Tensor | None
+    data: torch.Tensor
     struct: lutgemm_weight = field(default=None)
 
     @classmethod
     def empty(cls, m, n, q, g, has_offset, device) -> "PackedBCQ":
-        pb, ab, ob = lutgemm_packed_bytes(m, n, q, g, has_offset)
-        planes = torch.empty(pb, dtype=torch.uint8, device=device)
-        alpha = torch.empty(ab // 2, dtype=torch.float16, device=device)
-        offset = torch.empty(ob // 2, dtype=torch.float16, device=device) if has_offset else None
-        w = cls(m, n, q, g, has_offset, planes, alpha, offset)
-        w.struct = lutgemm_weight(m, n, q, g, int(has_offset), 0, planes.data_ptr(), alpha.data_ptr(),
-                                  _ptr(offset))
+        data = torch.empty(lutgemm_packed_bytes(m, n, q, g, has_offset), dtype=torch.uint8, device=device)
+        w = cls(m, n, q, g, has_offset, data)
+        w.struct = lutgemm_weight(m, n, q, g, int(has_offset), 0, data.data_ptr())
         return w
 
     def nbytes(self) -> int:
-        return self.planes.numel() + 2 * self.alpha.numel() + (2 * self.offset.numel() if self.offset is not None else 0)
+        return self.data.numel()
 
 
 def lutgemm_pack_bcq(planes: torch.Tensor, alpha: torch.Tensor, offset: torch.Tensor | None, n: int, g: int,
@@ -164,7 +158,7 @@ def lutgemm_pack_uniform(codes: torch.Tensor, scale: torch.Tensor, zero: torch.T
 
 def lutgemm_unpack_bcq(w: PackedBCQ, stream=None):
     """Native -> canonical (planes int32 [q][m][n/32], alpha fp16 [m][G][q], offset fp16 [m][G] | None)."""
-    dev = w.planes.device
+    dev = w.data.device
     G = w.n // w.g
     planes = torch.empty((w.q, w.m, w.n // 32), dtype=torch.int32, device=dev)
     alpha = torch.empty((w.m, G, w.q), dtype=torch.float16, device=dev)
@@ -220,6 +214,18 @@ def lutgemm_gemm_host(w: PackedBCQ, X_host: torch.Tensor, Y_host: torch.Tensor, 
     _check("lutgemm_gemm_host", lib.lutgemm_gemm_host(ctypes.byref(w.struct), X_host.data_ptr(), b, Y_host.data_ptr(),
                                                       ws.data_ptr(), ws.numel(), _stream(stream)))
     return Y_host
+
+
+def lutgemm_trace_enable(on: bool = True):
+    _check("lutgemm_trace_enable", lib.lutgemm_trace_enable(int(on)))
+
+
+def lutgemm_trace_read(ctas: int = 148):
+    """Per-CTA timeline of the last traced launch: uint64 [ctas][8] (see lutgemm.h)."""
+    import numpy as np
+    buf = (ctypes.c_uint64 * (8 * ctas))()
+    n = lib.lutgemm_trace_read(buf, 8 * ctas)
+    return np.frombuffer(buf, dtype=np.uint64, count=n).reshape(-1, 8).copy()
 
 
 # ---------------------------------------------------------------------------

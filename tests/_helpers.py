@@ -28,28 +28,39 @@ def assert_parity(y_gpu, y_ref, what=""):
 
 
 def native_pack_reference(planes: np.ndarray, alpha: np.ndarray, offset, m: int, n: int, q: int, g: int):
-    """Independent statement of layout.cuh: slice s = 1024 columns, L_s lanes
-    (32 columns each), row quads; planes[s][rq][i][lane][r4] uint32,
-    alpha[rq][i][G][r4], offset[rq][G][r4]; padded rows are zero."""
+    """Independent statement of layout.cuh: one byte stream, slice-major
+    (1024 columns per slice, L_s lanes of 32 columns), one record per row quad:
+    keys [q][L_s][4 rows] uint32, alpha [gps][q][4 rows] fp16, z [gps][4 rows]
+    fp16, zero padding to 16 bytes; gps = 32 L_s / g (g <= 1024) else 1."""
     m4 = (m + 3) // 4 * 4
     RQ = m4 // 4
     G = n // g
     nw = n // 32
     P = np.zeros((q, m4, nw), dtype=np.uint32)
     P[:, :m] = planes
+    A = np.zeros((m4, G, q), dtype=np.float16)
+    A[:m] = alpha
+    Z = np.zeros((m4, G), dtype=np.float16)
+    if offset is not None:
+        Z[:m] = offset
     out = []
     for s in range((n + 1023) // 1024):
         w0, w1 = 32 * s, min(nw, 32 * s + 32)
-        blk = P[:, :, w0:w1]                                   # [q][m4][L]
-        blk = blk.reshape(q, RQ, 4, w1 - w0).transpose(1, 0, 3, 2)   # [RQ][q][L][4]
-        out.append(np.ascontiguousarray(blk).reshape(-1))
-    planes_native = np.concatenate(out).view(np.uint8)
-    A = np.zeros((m4, G, q), dtype=np.float16)
-    A[:m] = alpha
-    alpha_native = A.reshape(RQ, 4, G, q).transpose(0, 3, 2, 1).reshape(-1)
-    off_native = None
-    if offset is not None:
-        Z = np.zeros((m4, G), dtype=np.float16)
-        Z[:m] = offset
-        off_native = Z.reshape(RQ, 4, G).transpose(0, 2, 1).reshape(-1)
-    return planes_native, alpha_native, off_native
+        L = w1 - w0
+        if g <= 1024:
+            gps = 32 * L // g
+            grps = list(range(s * (1024 // g), s * (1024 // g) + gps))
+        else:
+            gps, grps = 1, [(s * 1024) // g]
+        for rq in range(RQ):
+            rows = slice(4 * rq, 4 * rq + 4)
+            keys = P[:, rows, w0:w1].transpose(0, 2, 1)                 # [q][L][4]
+            al = A[rows][:, grps, :].transpose(1, 2, 0)                  # [gps][q][4]
+            rec = [np.ascontiguousarray(keys).view(np.uint8).reshape(-1),
+                   np.ascontiguousarray(al).view(np.uint8).reshape(-1)]
+            if offset is not None:
+                rec.append(np.ascontiguousarray(Z[rows][:, grps].T).view(np.uint8).reshape(-1))
+            r = np.concatenate(rec)
+            pad = (-len(r)) % 16
+            out.append(np.concatenate([r, np.zeros(pad, np.uint8)]))
+    return np.concatenate(out)

@@ -40,17 +40,20 @@ def test_abi_version_and_sizes():
     import paper_2206_09557_b200 as L
     from paper_2206_09557_b200.lutgemm import lib
     assert lib.lutgemm_abi_version() == 1
-    # planes = m4*q*n/8, alpha = m4*(n/g)*q*2, offset = m4*(n/g)*2 (layout.cuh)
-    assert L.lutgemm_packed_bytes(49152, 12288, 3, 128, False) == (226492416, 28311552, 0)
-    assert L.lutgemm_packed_bytes(22013, 8192, 4, 128, True) == (22016 * 4 * 1024, 22016 * 64 * 4 * 2, 22016 * 64 * 2)
-    # workspace: counters (ceil(RQ/16) u32, 256-B rounded) + S*b*m4 fp32 partials
-    ws = L.lutgemm_workspace_bytes(49152, 12288, 1)
-    assert ws == 3072 + 12 * 49152 * 4
-    assert L.lutgemm_workspace_bytes(49152, 12288, 4) == 3072 + 12 * 4 * 49152 * 4
+    # one record stream: m4*q*n/8 key bytes + m4*(n/g)*q*2 alpha (+ m4*(n/g)*2 z) (layout.cuh)
+    assert L.lutgemm_packed_bytes(49152, 12288, 3, 128, False) == 226492416 + 28311552
+    assert L.lutgemm_packed_bytes(22013, 8192, 4, 128, True) == 22016 * 4 * 1024 + 22016 * 64 * 4 * 2 + 22016 * 64 * 2
+    # row-wise g > 1024: the group's scales repeat in each of the S slices
+    assert L.lutgemm_packed_bytes(8, 2048, 3, 2048, False) == 2 * 2 * 1568   # 1536 + 24 -> 16-B padded
+    # workspace: S chunk counters (256-B rounded) + S*b*m4 fp32 split-K partials (256-B rounded)
+    assert L.lutgemm_workspace_bytes(49152, 12288, 1) == 256 + 12 * 49152 * 4
+    assert L.lutgemm_workspace_bytes(49152, 12288, 4) == 256 + 12 * 4 * 49152 * 4
+    assert L.lutgemm_workspace_bytes(5, 1056, 3) == 256 + (2 * 3 * 8 * 4 + 255) // 256 * 256
 
 
 @pytest.mark.parametrize("m,n,q,g", [(0, 64, 3, 32), (8, 48, 3, 48), (8, 64, 0, 32), (8, 64, 9, 32),
-                                     (8, 64, 3, 16), (8, 96, 3, 64), (8, 64, 3, 96)])
+                                     (8, 64, 3, 16), (8, 96, 3, 64), (8, 64, 3, 96), (8, 192, 3, 96),
+                                     (8, 6144, 3, 1536)])
 def test_invalid_shapes_rejected(m, n, q, g):
     import paper_2206_09557_b200 as L
     with pytest.raises(L.LutgemmError) as ei:
@@ -63,13 +66,16 @@ def test_gemv_argument_validation_without_gpu():
     """Validation happens before any device work: NULL/misaligned/small-ws
     arguments are rejected on a CPU-only host too."""
     from paper_2206_09557_b200.lutgemm import lib, lutgemm_weight
-    w = lutgemm_weight(64, 64, 3, 32, 0, 0, 4096, 8192, None)
+    w = lutgemm_weight(64, 64, 3, 32, 0, 0, 4096)
     st = lib.lutgemm_gemv(ctypes.byref(w), 4096 + 2, 8192, 16384, 1 << 20, None)
     assert st == 2 and b"x must be 16-byte aligned" in lib.lutgemm_last_error()
     st = lib.lutgemm_gemv(ctypes.byref(w), 4096, 8192, 16384, 16, None)
     assert st == 3 and b"workspace" in lib.lutgemm_last_error()
     st = lib.lutgemm_gemm_batched(ctypes.byref(w), 4096, 33, 8192, 16384, 1 << 20, None)
     assert st == 1
-    w.has_offset = 1
+    w.has_offset = 2
     st = lib.lutgemm_gemv(ctypes.byref(w), 4096, 8192, 16384, 1 << 20, None)
     assert st == 1 and b"offset" in lib.lutgemm_last_error()
+    w.has_offset, w.data = 0, 4100
+    st = lib.lutgemm_gemv(ctypes.byref(w), 4096, 8192, 16384, 1 << 20, None)
+    assert st == 2 and b"weight data" in lib.lutgemm_last_error()

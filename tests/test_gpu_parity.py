@@ -193,9 +193,10 @@ def test_llama_uniform_sampled(name):
     planes, alpha, z = O.uniform_to_bcq(u["codes"][rows], u["scale"][rows], u["zero"][rows], c["q"])
     ref = O.bcq_gemv(planes, O.store_fp16(alpha), O.store_fp16(z), X, c["n"], c["g"])[0]
     assert_parity(y[rows], ref, name)
-    # and against the uniform matrix itself (includes the fp16 storage of z, R17)
+    # against the uniform matrix itself: this adds the fp16 storage error of z
+    # (R17) to the kernel error, so only the aggregate rel-L2 bar applies here
     W = O.uniform_dequantize(u["codes"][rows], u["scale"][rows], u["zero"][rows], c["g"])
-    assert_parity(y[rows], (X.astype(np.float64) @ W.T)[0], name + "-uniform")
+    assert parity(y[rows], (X.astype(np.float64) @ W.T)[0])["rel_l2"] <= 2e-3
 
 
 def test_fc1_batched_32_sampled():
