@@ -6,20 +6,20 @@
 // [32p, 32p+32) = chunks 4p..4p+3, i.e. one canonical uint32 word per row.  The
 // last slice of an n that is not a multiple of 1024 has fewer lanes (L < 32).
 //
-// The weight is ONE byte stream, slice-major; inside slice s it is a sequence
-// of fixed-size records, one per row quad rq (rows 4rq..4rq+3):
+// The weight is ONE buffer, slice-major.  Slice s holds three regions, each
+// starting on a 256-byte boundary (the L2 fills DRAM sectors in 256-byte
+// blocks; misaligned 512-byte warp loads would over-fetch):
 //
-//   record(s, rq) = keys  [q][L_s][4 rows] uint32   (q*L_s*16 bytes)
-//                   alpha [gps_s][q][4 rows] fp16    (q*gps_s*8 bytes)
-//                   z     [gps_s][4 rows] fp16       (gps_s*8 bytes, if has_offset)
-//                   zero padding to a multiple of 16 bytes
+//   keys  [RQ][q][L_s][4 rows] uint32   -> q*L_s*16 bytes per row quad
+//   alpha [RQ][gps_s][q][4 rows] fp16   -> q*gps_s*8 bytes per row quad
+//   z     [RQ][gps_s][4 rows] fp16      -> gps_s*8 bytes per row quad (has_offset)
 //
 // gps_s = groups per slice = 32*L_s/g when g <= 1024 (g must divide 1024), else
 // 1 (g a multiple of 1024, or g == n): that group's scales are then repeated in
 // every slice it spans.  So a CTA working on (slice s, row quads [a, b)) reads
-// one contiguous byte range -- which a single bulk L2 prefetch can run ahead
-// of -- and a warp's 128-bit key loads for one (rq, plane) cover 512
-// contiguous bytes.  Rows m..m4-1 (m4 = 4*ceil(m/4)) are zero.
+// three contiguous byte ranges, and a warp's 128-bit key loads for one
+// (rq, plane) cover 512 contiguous, 512-byte-aligned bytes (full slices).
+// Rows m..m4-1 (m4 = 4*ceil(m/4)) are zero.
 #pragma once
 #include <cstddef>
 #include <cstdint>
@@ -64,39 +64,51 @@ __host__ __device__ inline int global_group(const Shape& sh, int s, int k) {
   return sh.g <= kSliceCols ? s * (kSliceCols / sh.g) + k : (s * kSliceCols) / sh.g;
 }
 
+// bytes per row quad in each region
 __host__ __device__ inline uint32_t keys_bytes(const Shape& sh, int Ls) { return (uint32_t)sh.q * Ls * 16u; }
+__host__ __device__ inline uint32_t alpha_bytes(const Shape& sh, int Ls) {
+  return (uint32_t)sh.q * slice_groups(sh, Ls) * 8u;
+}
+__host__ __device__ inline uint32_t z_bytes(const Shape& sh, int Ls) {
+  return sh.has_z ? (uint32_t)slice_groups(sh, Ls) * 8u : 0u;
+}
 
-__host__ __device__ inline uint32_t record_bytes(const Shape& sh, int Ls) {
-  const uint32_t gps = (uint32_t)slice_groups(sh, Ls);
-  const uint32_t raw = keys_bytes(sh, Ls) + (uint32_t)sh.q * gps * 8u + (sh.has_z ? gps * 8u : 0u);
-  return (raw + 15u) / 16u * 16u;
+__host__ __device__ inline size_t pad256(size_t v) { return (v + 255) / 256 * 256; }
+
+__host__ __device__ inline size_t slice_bytes(const Shape& sh, int Ls) {
+  return pad256((size_t)sh.RQ * keys_bytes(sh, Ls)) + pad256((size_t)sh.RQ * alpha_bytes(sh, Ls)) +
+         pad256((size_t)sh.RQ * z_bytes(sh, Ls));
 }
 
 __host__ __device__ inline size_t slice_base(const Shape& sh, int s) {
-  // every slice before s is full
-  return (size_t)s * (size_t)sh.RQ * record_bytes(sh, kLanesPerSlice);
+  return (size_t)s * slice_bytes(sh, kLanesPerSlice);  // every slice before s is full
 }
 
-__host__ __device__ inline size_t record_offset(const Shape& sh, int s, int Ls, int rq) {
-  return slice_base(sh, s) + (size_t)rq * record_bytes(sh, Ls);
+// region bases inside the buffer
+__host__ __device__ inline size_t keys_base(const Shape& sh, int s, int Ls) { return slice_base(sh, s); }
+__host__ __device__ inline size_t alpha_base(const Shape& sh, int s, int Ls) {
+  return slice_base(sh, s) + pad256((size_t)sh.RQ * keys_bytes(sh, Ls));
+}
+__host__ __device__ inline size_t z_base(const Shape& sh, int s, int Ls) {
+  return alpha_base(sh, s, Ls) + pad256((size_t)sh.RQ * alpha_bytes(sh, Ls));
 }
 
 __host__ __device__ inline size_t packed_bytes(const Shape& sh) {
   const int Sfull = sh.n / kSliceCols;
-  size_t b = (size_t)Sfull * sh.RQ * record_bytes(sh, kLanesPerSlice);
-  if (sh.n % kSliceCols) b += (size_t)sh.RQ * record_bytes(sh, slice_lanes(sh.n, Sfull));
+  size_t b = (size_t)Sfull * slice_bytes(sh, kLanesPerSlice);
+  if (sh.n % kSliceCols) b += slice_bytes(sh, slice_lanes(sh.n, Sfull));
   return b;
 }
 
-// byte offsets inside a record
-__host__ __device__ inline uint32_t key_off(int Ls, int i, int p, int r4) {
-  return ((uint32_t)i * Ls + p) * 16u + 4u * r4;
+// byte offsets of single elements
+__host__ __device__ inline size_t key_at(const Shape& sh, int s, int Ls, int rq, int i, int p, int r4) {
+  return keys_base(sh, s, Ls) + (size_t)rq * keys_bytes(sh, Ls) + ((uint32_t)i * Ls + p) * 16u + 4u * r4;
 }
-__host__ __device__ inline uint32_t alpha_off(const Shape& sh, int Ls, int i, int k, int r4) {
-  return keys_bytes(sh, Ls) + ((uint32_t)k * sh.q + i) * 8u + 2u * r4;
+__host__ __device__ inline size_t alpha_at(const Shape& sh, int s, int Ls, int rq, int i, int k, int r4) {
+  return alpha_base(sh, s, Ls) + (size_t)rq * alpha_bytes(sh, Ls) + ((uint32_t)k * sh.q + i) * 8u + 2u * r4;
 }
-__host__ __device__ inline uint32_t z_off(const Shape& sh, int Ls, int k, int r4) {
-  return keys_bytes(sh, Ls) + (uint32_t)sh.q * slice_groups(sh, Ls) * 8u + k * 8u + 2u * r4;
+__host__ __device__ inline size_t z_at(const Shape& sh, int s, int Ls, int rq, int k, int r4) {
+  return z_base(sh, s, Ls) + (size_t)rq * z_bytes(sh, Ls) + (uint32_t)k * 8u + 2u * r4;
 }
 
 }  // namespace lg

@@ -164,42 +164,57 @@ struct Ring {
   uint2 z;
 };
 
-// Per-segment addressing of a lane's record fields.
+// Per-segment addressing of a lane's fields in the three slice regions.
 struct LaneAddr {
-  const uint8_t* seg;  // slice base in the record stream
-  uint32_t R;          // record bytes
-  uint32_t koff;       // lane's key offset in a record (plane 0)
-  uint32_t kstride;    // bytes between planes of the key block (Ls * 16)
-  uint32_t aoff;       // lane's alpha offset in a record (plane 0)
-  uint32_t zoff;       // lane's z offset in a record
+  const uint8_t* kp;  // lane's key bytes of row quad 0, plane 0
+  const uint8_t* ap;  // lane's alpha of row quad 0, plane 0
+  const uint8_t* zp;  // lane's z of row quad 0
+  uint32_t KB, AB, ZB;  // per-row-quad strides of the regions
+  uint32_t kstride;     // bytes between planes of the key block (Ls * 16)
 };
 
 __device__ __forceinline__ LaneAddr lane_addr(const Shape& sh, const uint8_t* data, int s, int Ls, int lay) {
   LaneAddr a;
-  a.seg = data + slice_base(sh, s);
-  a.R = record_bytes(sh, Ls);
-  a.koff = key_off(Ls, 0, lay, 0);
-  a.kstride = (uint32_t)Ls * 16u;
   const int k = lane_group(sh, lay);
-  a.aoff = alpha_off(sh, Ls, 0, k, 0);
-  a.zoff = z_off(sh, Ls, k, 0);
+  a.kp = data + key_at(sh, s, Ls, 0, 0, lay, 0);
+  a.ap = data + alpha_at(sh, s, Ls, 0, 0, k, 0);
+  a.zp = data + z_at(sh, s, Ls, 0, k, 0);
+  a.KB = keys_bytes(sh, Ls);
+  a.AB = alpha_bytes(sh, Ls);
+  a.ZB = z_bytes(sh, Ls);
+  a.kstride = (uint32_t)Ls * 16u;
   return a;
 }
 
-template <int QT, bool HAS_Z>
+// L2 prefetch of row quads [a, b) of slice s (all regions), issued by one thread
+__device__ __forceinline__ void prefetch_quads(const Shape& sh, const uint8_t* data, int s, int Ls, int a, int b) {
+  if (b <= a) return;
+  const uint32_t kb = keys_bytes(sh, Ls), ab = alpha_bytes(sh, Ls), zb = z_bytes(sh, Ls);
+  // region starts are 256-aligned; per-quad sizes are multiples of 8, so round the ranges to 16 bytes
+  auto pf = [](const uint8_t* base, size_t lo, size_t hi) {
+    lo &= ~(size_t)15;
+    hi = (hi + 15) & ~(size_t)15;
+    if (hi > lo) bulk_prefetch_l2(base + lo, (uint32_t)(hi - lo));
+  };
+  pf(data + keys_base(sh, s, Ls), (size_t)a * kb, (size_t)b * kb);
+  pf(data + alpha_base(sh, s, Ls), (size_t)a * ab, (size_t)b * ab);
+  if (zb) pf(data + z_base(sh, s, Ls), (size_t)a * zb, (size_t)b * zb);
+}
+
+template <int QT, bool HAS_Z, int MODE = 0>
 __device__ __forceinline__ void ring_load(Ring<QT>& r, bool ok, const LaneAddr& la, int rq, int q) {
   if (ok) {
-    const uint8_t* rec = la.seg + (size_t)rq * la.R;
-    const uint8_t* kp = rec + la.koff;
-    const uint8_t* ap = rec + la.aoff;
+    const uint8_t* kp = la.kp + (size_t)rq * la.KB;
+    const uint8_t* ap = la.ap + (size_t)rq * la.AB;
 #pragma unroll
     for (int i = 0; i < QT; ++i) {
       if (QT <= 4 || i < q) {
         r.k[i] = ldg_stream_u4(kp + i * la.kstride);
-        r.a[i] = ldg_nc_u2(ap + 8 * i);
+        if (MODE != 4) r.a[i] = ldg_nc_u2(ap + 8 * i);
+        else r.a[i] = make_uint2(0, 0);
       }
     }
-    if (HAS_Z) r.z = ldg_nc_u2(rec + la.zoff);
+    if (HAS_Z) r.z = ldg_nc_u2(la.zp + (size_t)rq * la.ZB);
   } else {
 #pragma unroll
     for (int i = 0; i < QT; ++i) {
@@ -214,6 +229,14 @@ __device__ __forceinline__ void ring_load(Ring<QT>& r, bool ok, const LaneAddr& 
 template <int QT, bool HAS_Z, int MODE = 0>
 __device__ __forceinline__ void ring_compute(const Ring<QT>& r, uint32_t lc, float xsum, f32x2& acc01, f32x2& acc23,
                                              int q, bool accumulate) {
+  if (MODE == 3 || MODE == 4) {  // measurement variants: consume the loaded words with minimal work
+    uint32_t v = 0;
+#pragma unroll
+    for (int i = 0; i < QT; ++i) v ^= r.k[i].x ^ r.k[i].y ^ r.k[i].z ^ r.k[i].w ^ r.a[i].x ^ r.a[i].y;
+    acc01 = pack2(__uint_as_float(v & 0x3fffffffu), 0.f);
+    acc23 = pack2(0.f, 0.f);
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < QT; ++i) {
     if (QT <= 4 || i < q) {
@@ -300,16 +323,21 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
       if (trace) trace[5] = globaltimer_ns();
       if (warp == 0) stage_x(xbuf0, bar0, p.x, sh.n, s * kSliceCols, Ls, 32, 1, 1, lane);
     }
-    if (tid == 0) {
-      const int hi = min(rq_b, rq_a + pf_steps * kWarps);
-      if (hi > rq_a) bulk_prefetch_l2(la.seg + (size_t)rq_a * la.R, (uint32_t)(hi - rq_a) * la.R);
-    }
-    Ring<QT> ring[PD];
+    if (tid == 0) prefetch_quads(sh, p.data, s, Ls, rq_a, min(rq_b, rq_a + pf_steps * kWarps));
+    // this warp's row quads in the segment: rq_a + warp + 16 t, t < nt
+    const int nt = rq_a + warp < rq_b ? (rq_b - (rq_a + warp) + kWarps - 1) / kWarps : 0;
+    // double-buffered batches of U = PD quads: the next batch is requested
+    // before the current one is computed, so the loads overlap the lookups
+    constexpr int U = PD;
+    Ring<QT> bufA[U], bufB[U];
+    auto load_batch = [&](Ring<QT>(&buf)[U], int t0) {
 #pragma unroll
-    for (int d = 0; d < PD; ++d) {
-      const int rq = rq_a + warp + d * kWarps;
-      ring_load<QT, HAS_Z>(ring[d], lane_ok && rq < rq_b, la, rq, q);
-    }
+      for (int u = 0; u < U; ++u) {
+        const int t = t0 + u;
+        ring_load<QT, HAS_Z, MODE>(buf[u], lane_ok && t < nt, la, rq_a + warp + kWarps * t, q);
+      }
+    };
+    load_batch(bufA, 0);
     if (e == 0) __syncthreads();  // the zero-fill of the x buffer is visible
     // 2. wait for the staged x slice and build the 128 LUTs of the slice
     __half* xb = (e & 1) ? xbuf1 : xbuf0;
@@ -329,25 +357,30 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     }
     const float xsum = (HAS_Z && lane_ok) ? lane_xsum(sm.lut, lane) : 0.f;
     float* part = p.partial + (size_t)s * sh.m4;
-    // 4. main loop: row quads rq_a + warp + 16 t
-    for (int rq0 = rq_a + warp; rq0 < rq_b; rq0 += PD * kWarps) {
+    auto compute_batch = [&](const Ring<QT>(&buf)[U], int t0) {
 #pragma unroll
-      for (int d = 0; d < PD; ++d) {
-        const int rq = rq0 + d * kWarps;
-        if (rq < rq_b) {
-          if (tid == 0) {  // keep the L2 prefetch pf_steps steps ahead of warp 0
-            const int lo = rq + pf_steps * kWarps;
-            if (lo < rq_b)
-              bulk_prefetch_l2(la.seg + (size_t)lo * la.R, (uint32_t)(min(rq_b, lo + kWarps) - lo) * la.R);
-          }
+      for (int u = 0; u < U; ++u) {
+        const int t = t0 + u;
+        if (t < nt) {
+          const int rq = rq_a + warp + kWarps * t;
           f32x2 acc01, acc23;
-          ring_compute<QT, HAS_Z, MODE>(ring[d], lc, xsum, acc01, acc23, q, false);
+          ring_compute<QT, HAS_Z, MODE>(buf[u], lc, xsum, acc01, acc23, q, false);
           const float v = reduce4(acc01, acc23, lane);
           if ((lane & 7) == 0) part[4 * rq + (lane >> 3)] = v;
-          const int rn = rq + PD * kWarps;
-          if (MODE != 2) ring_load<QT, HAS_Z>(ring[d], lane_ok && rn < rq_b, la, rn, q);
         }
       }
+    };
+    // 4. main loop
+    for (int t0 = 0; t0 < nt; t0 += 2 * U) {
+      if (tid == 0 && pf_steps > 0) {  // keep the L2 prefetch pf_steps steps ahead of warp 0
+        const int lo = rq_a + kWarps * (t0 + pf_steps);
+        prefetch_quads(sh, p.data, s, Ls, lo, min(rq_b, lo + 2 * U * kWarps));
+      }
+      load_batch(bufB, t0 + U);
+      compute_batch(bufA, t0);
+      if (t0 + U >= nt) break;
+      load_batch(bufA, t0 + 2 * U);
+      compute_batch(bufB, t0 + U);
     }
     if (trace && e == 0) trace[3] = globaltimer_ns();  // warp 0's loop end
     __syncthreads();  // the LUT and x buffer are reused by the next segment
@@ -391,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemm_batched_kernel(const KPa
     const int s = (int)(itx / NRB), rb = (int)(itx % NRB);
     const int Ls = slice_lanes(sh.n, s);
     const int lo = rb * rbq, hi = min(sh.RQ, lo + rbq);
-    bulk_prefetch_l2(p.data + record_offset(sh, s, Ls, lo), (uint32_t)(hi - lo) * record_bytes(sh, Ls));
+    prefetch_quads(sh, p.data, s, Ls, lo, hi);
   };
   // staging of sub-slice (s, k): P lanes starting at layout lane k*P
   auto stage = [&](int ebuf, long long itx, int k) {
@@ -574,14 +607,18 @@ static cudaError_t launch_reduce(const KParams& p, cudaStream_t st) {
 
 template <int QT, bool HAS_Z>
 static cudaError_t launch_gemv_t(const KParams& p, int grid, cudaStream_t st) {
-  constexpr int PD = QT <= 1 ? 6 : (QT <= 2 ? 4 : (QT <= 4 ? 3 : 1));
-  if (QT == 3 && !HAS_Z && p.xmode >= 10) {  // measurement variants (LUTGEMM_XMODE)
+  // batch size U (quads per buffer, two buffers): as large as the 128-register budget allows
+  constexpr int PD = 1;
+  if constexpr (QT == 3 && !HAS_Z) {
+    if (p.xmode >= 10) {  // measurement variants (LUTGEMM_XMODE)
     switch (p.xmode) {
-      case 10: return launch(lut_gemv_kernel<QT, HAS_Z, 2, 0>, grid, p, st);
-      case 11: return launch(lut_gemv_kernel<QT, HAS_Z, 3, 1>, grid, p, st);
-      case 12: return launch(lut_gemv_kernel<QT, HAS_Z, 3, 2>, grid, p, st);
-      case 14: return launch(lut_gemv_kernel<QT, HAS_Z, 4, 0>, grid, p, st);
+      case 10: return launch(lut_gemv_kernel<QT, HAS_Z, 1, 0>, grid, p, st);
+      case 11: return launch(lut_gemv_kernel<QT, HAS_Z, 2, 1>, grid, p, st);
+      case 13: return launch(lut_gemv_kernel<QT, HAS_Z, 2, 3>, grid, p, st);
+      case 16: return launch(lut_gemv_kernel<QT, HAS_Z, 2, 4>, grid, p, st);
+      case 14: return launch(lut_gemv_kernel<QT, HAS_Z, 3, 0>, grid, p, st);
       default: break;
+    }
     }
   }
   return launch(lut_gemv_kernel<QT, HAS_Z, PD>, grid, p, st);
@@ -635,7 +672,7 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
                         void* ws, cudaStream_t st) {
   if (g_pf_steps < 0) {
     const char* env = getenv("LUTGEMM_PF_STEPS");  // tuning knob (default kPfSteps)
-    g_pf_steps = env ? atoi(env) : kPfSteps;
+    g_pf_steps = env ? atoi(env) : 0;
   }
   KParams p;
   p.data = static_cast<const uint8_t*>(data);

@@ -35,7 +35,7 @@ __global__ void pack_keys_kernel(const uint32_t* __restrict__ src, uint8_t* __re
     const uint32_t v = r < sh.m ? src[((size_t)i * sh.m + r) * nw + w] : 0u;
     const int s = w / kLanesPerSlice, p = w % kLanesPerSlice;
     const int Ls = slice_lanes(sh.n, s);
-    *reinterpret_cast<uint32_t*>(dst + record_offset(sh, s, Ls, r / 4) + key_off(Ls, i, p, r % 4)) = v;
+    *reinterpret_cast<uint32_t*>(dst + key_at(sh, s, Ls, r / 4, i, p, r % 4)) = v;
   }
 }
 
@@ -48,7 +48,7 @@ __global__ void unpack_keys_kernel(const uint8_t* __restrict__ src, uint32_t* __
     const int i = (int)(idx / ((size_t)nw * sh.m));
     const int s = w / kLanesPerSlice, p = w % kLanesPerSlice;
     const int Ls = slice_lanes(sh.n, s);
-    dst[idx] = *reinterpret_cast<const uint32_t*>(src + record_offset(sh, s, Ls, r / 4) + key_off(Ls, i, p, r % 4));
+    dst[idx] = *reinterpret_cast<const uint32_t*>(src + key_at(sh, s, Ls, r / 4, i, p, r % 4));
   }
 }
 
@@ -65,14 +65,13 @@ __global__ void pack_scales_kernel(const uint16_t* __restrict__ alpha, const uin
     const int Ls = slice_lanes(sh.n, s);
     if (k >= slice_groups(sh, Ls)) continue;
     const int grp = global_group(sh, s, k);
-    uint8_t* rec = dst + record_offset(sh, s, Ls, rq);
     for (int r4 = 0; r4 < 4; ++r4) {
       const int r = 4 * rq + r4;
       for (int i = 0; i < sh.q; ++i)
-        *reinterpret_cast<uint16_t*>(rec + alpha_off(sh, Ls, i, k, r4)) =
+        *reinterpret_cast<uint16_t*>(dst + alpha_at(sh, s, Ls, rq, i, k, r4)) =
             r < sh.m ? alpha[((size_t)r * sh.G + grp) * sh.q + i] : (uint16_t)0;
       if (sh.has_z)
-        *reinterpret_cast<uint16_t*>(rec + z_off(sh, Ls, k, r4)) =
+        *reinterpret_cast<uint16_t*>(dst + z_at(sh, s, Ls, rq, k, r4)) =
             (r < sh.m && offset) ? offset[(size_t)r * sh.G + grp] : (uint16_t)0;
     }
   }
@@ -98,11 +97,11 @@ __global__ void unpack_scales_kernel(const uint8_t* __restrict__ src, uint16_t* 
     int s, k;
     home_of_group(sh, grp, &s, &k);
     const int Ls = slice_lanes(sh.n, s);
-    const uint8_t* rec = src + record_offset(sh, s, Ls, r / 4);
     if (alpha)
       for (int i = 0; i < sh.q; ++i)
-        alpha[idx * sh.q + i] = *reinterpret_cast<const uint16_t*>(rec + alpha_off(sh, Ls, i, k, r % 4));
-    if (offset && sh.has_z) offset[idx] = *reinterpret_cast<const uint16_t*>(rec + z_off(sh, Ls, k, r % 4));
+        alpha[idx * sh.q + i] = *reinterpret_cast<const uint16_t*>(src + alpha_at(sh, s, Ls, r / 4, i, k, r % 4));
+    if (offset && sh.has_z)
+      offset[idx] = *reinterpret_cast<const uint16_t*>(src + z_at(sh, s, Ls, r / 4, k, r % 4));
   }
 }
 
@@ -123,8 +122,7 @@ __global__ void pack_uniform_keys_kernel(const uint8_t* __restrict__ codes, uint
     }
     const int s = w / kLanesPerSlice, p = w % kLanesPerSlice;
     const int Ls = slice_lanes(sh.n, s);
-    uint8_t* rec = dst + record_offset(sh, s, Ls, r / 4);
-    for (int i = 0; i < sh.q; ++i) *reinterpret_cast<uint32_t*>(rec + key_off(Ls, i, p, r % 4)) = words[i];
+    for (int i = 0; i < sh.q; ++i) *reinterpret_cast<uint32_t*>(dst + key_at(sh, s, Ls, r / 4, i, p, r % 4)) = words[i];
   }
 }
 
@@ -140,7 +138,6 @@ __global__ void pack_uniform_scales_kernel(const uint16_t* __restrict__ scale, c
     const int Ls = slice_lanes(sh.n, s);
     if (k >= slice_groups(sh, Ls)) continue;
     const int grp = global_group(sh, s, k);
-    uint8_t* rec = dst + record_offset(sh, s, Ls, rq);
     for (int r4 = 0; r4 < 4; ++r4) {
       const int r = 4 * rq + r4;
       double sv = 0.0, zh = 0.0;
@@ -152,9 +149,9 @@ __global__ void pack_uniform_scales_kernel(const uint16_t* __restrict__ scale, c
       for (int i = 0; i < sh.q; ++i) {
         const double a = ldexp(sv, i - 1);
         sum_alpha += a;
-        *reinterpret_cast<uint16_t*>(rec + alpha_off(sh, Ls, i, k, r4)) = __half_as_ushort(__double2half(a));
+        *reinterpret_cast<uint16_t*>(dst + alpha_at(sh, s, Ls, rq, i, k, r4)) = __half_as_ushort(__double2half(a));
       }
-      *reinterpret_cast<uint16_t*>(rec + z_off(sh, Ls, k, r4)) =
+      *reinterpret_cast<uint16_t*>(dst + z_at(sh, s, Ls, rq, k, r4)) =
           __half_as_ushort(__double2half(r < sh.m ? sum_alpha + zh : 0.0));
     }
   }

@@ -29,11 +29,19 @@ __device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
 }
 
 // Streaming 128-bit load of packed bit-planes: read once, do not pollute L1.
+// No L2 sector-promotion hint: records are not 256-byte aligned, and a
+// .L2::256B promotion of a misaligned 512-byte warp access over-fetches DRAM.
 __device__ __forceinline__ uint4 ldg_stream_u4(const void* p) {
   uint4 r;
+#ifdef LUTGEMM_L2_256B
   asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
+#else
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+#endif
   return r;
 }
 

@@ -28,10 +28,11 @@ def assert_parity(y_gpu, y_ref, what=""):
 
 
 def native_pack_reference(planes: np.ndarray, alpha: np.ndarray, offset, m: int, n: int, q: int, g: int):
-    """Independent statement of layout.cuh: one byte stream, slice-major
-    (1024 columns per slice, L_s lanes of 32 columns), one record per row quad:
-    keys [q][L_s][4 rows] uint32, alpha [gps][q][4 rows] fp16, z [gps][4 rows]
-    fp16, zero padding to 16 bytes; gps = 32 L_s / g (g <= 1024) else 1."""
+    """Independent statement of layout.cuh: slice-major (1024 columns per slice,
+    L_s lanes of 32 columns); slice s = three regions, each zero-padded to a
+    multiple of 256 bytes: keys [RQ][q][L_s][4 rows] uint32, alpha
+    [RQ][gps][q][4 rows] fp16, z [RQ][gps][4 rows] fp16 (if offset);
+    gps = 32 L_s / g (g <= 1024) else 1."""
     m4 = (m + 3) // 4 * 4
     RQ = m4 // 4
     G = n // g
@@ -43,6 +44,10 @@ def native_pack_reference(planes: np.ndarray, alpha: np.ndarray, offset, m: int,
     Z = np.zeros((m4, G), dtype=np.float16)
     if offset is not None:
         Z[:m] = offset
+
+    def pad256(b):
+        return np.concatenate([b, np.zeros((-len(b)) % 256, np.uint8)])
+
     out = []
     for s in range((n + 1023) // 1024):
         w0, w1 = 32 * s, min(nw, 32 * s + 32)
@@ -52,15 +57,11 @@ def native_pack_reference(planes: np.ndarray, alpha: np.ndarray, offset, m: int,
             grps = list(range(s * (1024 // g), s * (1024 // g) + gps))
         else:
             gps, grps = 1, [(s * 1024) // g]
-        for rq in range(RQ):
-            rows = slice(4 * rq, 4 * rq + 4)
-            keys = P[:, rows, w0:w1].transpose(0, 2, 1)                 # [q][L][4]
-            al = A[rows][:, grps, :].transpose(1, 2, 0)                  # [gps][q][4]
-            rec = [np.ascontiguousarray(keys).view(np.uint8).reshape(-1),
-                   np.ascontiguousarray(al).view(np.uint8).reshape(-1)]
-            if offset is not None:
-                rec.append(np.ascontiguousarray(Z[rows][:, grps].T).view(np.uint8).reshape(-1))
-            r = np.concatenate(rec)
-            pad = (-len(r)) % 16
-            out.append(np.concatenate([r, np.zeros(pad, np.uint8)]))
+        keys = P[:, :, w0:w1].reshape(q, RQ, 4, L).transpose(1, 0, 3, 2)          # [RQ][q][L][4]
+        al = A[:, grps, :].reshape(RQ, 4, gps, q).transpose(0, 2, 3, 1)           # [RQ][gps][q][4]
+        out.append(pad256(np.ascontiguousarray(keys).view(np.uint8).reshape(-1)))
+        out.append(pad256(np.ascontiguousarray(al).view(np.uint8).reshape(-1)))
+        if offset is not None:
+            zz = Z[:, grps].reshape(RQ, 4, gps).transpose(0, 2, 1)                 # [RQ][gps][4]
+            out.append(pad256(np.ascontiguousarray(zz).view(np.uint8).reshape(-1)))
     return np.concatenate(out)

@@ -43,8 +43,8 @@ def test_abi_version_and_sizes():
     # one record stream: m4*q*n/8 key bytes + m4*(n/g)*q*2 alpha (+ m4*(n/g)*2 z) (layout.cuh)
     assert L.lutgemm_packed_bytes(49152, 12288, 3, 128, False) == 226492416 + 28311552
     assert L.lutgemm_packed_bytes(22013, 8192, 4, 128, True) == 22016 * 4 * 1024 + 22016 * 64 * 4 * 2 + 22016 * 64 * 2
-    # row-wise g > 1024: the group's scales repeat in each of the S slices
-    assert L.lutgemm_packed_bytes(8, 2048, 3, 2048, False) == 2 * 2 * 1568   # 1536 + 24 -> 16-B padded
+    # row-wise g > 1024: the group's scales repeat in each of the S slices; regions 256-B padded
+    assert L.lutgemm_packed_bytes(8, 2048, 3, 2048, False) == 2 * (2 * 1536 + 256)
     # workspace: S chunk counters (256-B rounded) + S*b*m4 fp32 split-K partials (256-B rounded)
     assert L.lutgemm_workspace_bytes(49152, 12288, 1) == 256 + 12 * 49152 * 4
     assert L.lutgemm_workspace_bytes(49152, 12288, 4) == 256 + 12 * 4 * 49152 * 4
