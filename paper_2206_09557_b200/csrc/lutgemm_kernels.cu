@@ -326,18 +326,16 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     if (tid == 0) prefetch_quads(sh, p.data, s, Ls, rq_a, min(rq_b, rq_a + pf_steps * kWarps));
     // this warp's row quads in the segment: rq_a + warp + 16 t, t < nt
     const int nt = rq_a + warp < rq_b ? (rq_b - (rq_a + warp) + kWarps - 1) / kWarps : 0;
-    // double-buffered batches of U = PD quads: the next batch is requested
-    // before the current one is computed, so the loads overlap the lookups
-    constexpr int U = PD;
-    Ring<QT> bufA[U], bufB[U];
-    auto load_batch = [&](Ring<QT>(&buf)[U], int t0) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int t = t0 + u;
-        ring_load<QT, HAS_Z, MODE>(buf[u], lane_ok && t < nt, la, rq_a + warp + kWarps * t, q);
-      }
+    // a ring of NB = PD + 1 single-quad buffers: the load for quad t + PD is
+    // issued BEFORE quad t is computed (the lookups and the reduction's
+    // shuffles would otherwise delay it), so PD quads are always in flight
+    constexpr int NB = PD + 1;
+    Ring<QT> buf[NB];
+    auto load_quad = [&](Ring<QT>& b, int t) {
+      ring_load<QT, HAS_Z, MODE>(b, lane_ok && t < nt, la, rq_a + warp + kWarps * t, q);
     };
-    load_batch(bufA, 0);
+#pragma unroll
+    for (int d = 0; d < PD; ++d) load_quad(buf[d], d);
     if (e == 0) __syncthreads();  // the zero-fill of the x buffer is visible
     // 2. wait for the staged x slice and build the 128 LUTs of the slice
     __half* xb = (e & 1) ? xbuf1 : xbuf0;
@@ -357,30 +355,24 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     }
     const float xsum = (HAS_Z && lane_ok) ? lane_xsum(sm.lut, lane) : 0.f;
     float* part = p.partial + (size_t)s * sh.m4;
-    auto compute_batch = [&](const Ring<QT>(&buf)[U], int t0) {
+    // 4. main loop
+    for (int t0 = 0; t0 < nt; t0 += NB) {
+      if (tid == 0 && pf_steps > 0) {  // optional L2 prefetch pf_steps steps ahead of warp 0
+        const int lo = rq_a + kWarps * (t0 + pf_steps);
+        prefetch_quads(sh, p.data, s, Ls, lo, min(rq_b, lo + NB * kWarps));
+      }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int t = t0 + u;
+      for (int d = 0; d < NB; ++d) {
+        const int t = t0 + d;
         if (t < nt) {
+          load_quad(buf[(d + PD) % NB], t + PD);
           const int rq = rq_a + warp + kWarps * t;
           f32x2 acc01, acc23;
-          ring_compute<QT, HAS_Z, MODE>(buf[u], lc, xsum, acc01, acc23, q, false);
+          ring_compute<QT, HAS_Z, MODE>(buf[d], lc, xsum, acc01, acc23, q, false);
           const float v = reduce4(acc01, acc23, lane);
           if ((lane & 7) == 0) part[4 * rq + (lane >> 3)] = v;
         }
       }
-    };
-    // 4. main loop
-    for (int t0 = 0; t0 < nt; t0 += 2 * U) {
-      if (tid == 0 && pf_steps > 0) {  // keep the L2 prefetch pf_steps steps ahead of warp 0
-        const int lo = rq_a + kWarps * (t0 + pf_steps);
-        prefetch_quads(sh, p.data, s, Ls, lo, min(rq_b, lo + 2 * U * kWarps));
-      }
-      load_batch(bufB, t0 + U);
-      compute_batch(bufA, t0);
-      if (t0 + U >= nt) break;
-      load_batch(bufA, t0 + 2 * U);
-      compute_batch(bufB, t0 + U);
     }
     if (trace && e == 0) trace[3] = globaltimer_ns();  // warp 0's loop end
     __syncthreads();  // the LUT and x buffer are reused by the next segment
@@ -607,8 +599,8 @@ static cudaError_t launch_reduce(const KParams& p, cudaStream_t st) {
 
 template <int QT, bool HAS_Z>
 static cudaError_t launch_gemv_t(const KParams& p, int grid, cudaStream_t st) {
-  // batch size U (quads per buffer, two buffers): as large as the 128-register budget allows
-  constexpr int PD = 1;
+  // quads in flight per warp while one is computed (ring of PD + 1 buffers)
+  constexpr int PD = QT <= 2 ? 3 : (QT <= 4 ? 2 : 1);
   if constexpr (QT == 3 && !HAS_Z) {
     if (p.xmode >= 10) {  // measurement variants (LUTGEMM_XMODE)
     switch (p.xmode) {
@@ -617,6 +609,7 @@ static cudaError_t launch_gemv_t(const KParams& p, int grid, cudaStream_t st) {
       case 13: return launch(lut_gemv_kernel<QT, HAS_Z, 2, 3>, grid, p, st);
       case 16: return launch(lut_gemv_kernel<QT, HAS_Z, 2, 4>, grid, p, st);
       case 14: return launch(lut_gemv_kernel<QT, HAS_Z, 3, 0>, grid, p, st);
+      case 18: return launch(lut_gemv_kernel<QT, HAS_Z, 4, 0>, grid, p, st);
       default: break;
     }
     }
