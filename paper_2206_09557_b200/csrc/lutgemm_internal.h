@@ -16,12 +16,13 @@ struct KParams {
   __half* y;         // [b][m] fp16 output (or null)
   float* yf;         // [b][m] fp32 output (or null)
   float* partial;    // [S][b][m4] split-K partials
-  unsigned* counters;  // [S] GEMV chunk counters (zero between launches)
+  unsigned* counters;  // GEMV fused mode: arrive/depart counters per row-quad group (zero between launches)
   Shape sh;
   int b;
   int bl;            // log2 of the table-bank count B >= b
   int pf_steps;      // GEMV: L2 prefetch distance in 16-quad steps
   int xmode;         // experiment knob (0 default)
+  int fused_J;       // GEMV: CTAs per slice in the fused-reduction mode (0: separate reduction kernel)
   long long items;
   unsigned long long* trace;  // optional per-CTA timeline (kTraceSlots u64 per CTA), or null
 };

@@ -52,6 +52,7 @@ constexpr int kMiscBytes = 8192;       // x double buffer (2 x 2 KB) + mbarriers
 constexpr int kSmemBytes = 3 * 65536;  // LUT (128 KB) on a 64 KB boundary + misc, for any base
 constexpr int kPfSteps = 8;            // GEMV: L2 prefetch distance in 16-quad steps
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kFusedMaxJ = 256;        // max CTAs per slice in the fused-reduction mode
 
 struct SmemMap {
   uint32_t lut;     // shared-window address of the LUT (multiple of 64 KB)
@@ -280,14 +281,24 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
   const int warp = __shfl_sync(kFull, tid >> 5, 0);  // warp-uniform for the compiler
   const Shape sh = p.sh;
   const int q = QT <= 4 ? QT : sh.q;
-  const long long it0 = p.items * blockIdx.x / gridDim.x;
-  const long long it1 = p.items * (blockIdx.x + 1) / gridDim.x;
+  // work: a contiguous range of the S*RQ (slice, row-quad) items; in the fused
+  // mode CTA c owns slice c / J, row-quad group c % J (one segment)
+  const int J = p.fused_J;
+  long long it0, it1;
+  if (J > 0) {
+    const int fs = blockIdx.x / J, fj = blockIdx.x % J;
+    it0 = (long long)fs * sh.RQ + (long long)sh.RQ * fj / J;
+    it1 = (long long)fs * sh.RQ + (long long)sh.RQ * (fj + 1) / J;
+  } else {
+    it0 = p.items * blockIdx.x / gridDim.x;
+    it1 = p.items * (blockIdx.x + 1) / gridDim.x;
+  }
   unsigned long long* trace = (p.trace && tid == 0) ? p.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
   if (trace) {
     trace[0] = globaltimer_ns();
     trace[7] = smid();
   }
-  if (it0 >= it1) return;
+  if (it0 >= it1 && J == 0) return;
 
   const SmemMap sm = map_smem(smem);
   __half* xbuf0 = reinterpret_cast<__half*>(sm.misc_p);
@@ -381,7 +392,46 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     ++e;
   }
   if (trace) trace[7] |= (unsigned long long)e << 32;  // segments processed
-  pdl_launch_dependents();  // the reduction kernel may now be scheduled
+  if (J > 0) {
+    // Fused cross-slice reduction: the S CTAs that share row-quad group fj
+    // (one per slice) meet at a counter -- all CTAs of the grid are resident
+    // (grid <= #SMs, one CTA per SM) -- then each sums its 1/S share of the
+    // group's rows over the S slices in slice order (deterministic, R11).
+    const int fs = blockIdx.x / J, fj = blockIdx.x % J;
+    unsigned* arrive = p.counters + fj;
+    unsigned* depart = p.counters + kFusedMaxJ + fj;
+    if (e == 0) pdl_wait();  // (an empty range never reached the wait above)
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      atomicAdd(arrive, 1u);
+      while (ld_acquire_u32(arrive) < (unsigned)sh.S) __nanosleep(32);
+    }
+    __syncthreads();
+    const int g0 = (int)((long long)sh.RQ * fj / J), g1 = (int)((long long)sh.RQ * (fj + 1) / J);
+    const int r0 = 4 * (g0 + (int)((long long)(g1 - g0) * fs / sh.S));
+    const int r1 = min(sh.m, 4 * (g0 + (int)((long long)(g1 - g0) * (fs + 1) / sh.S)));
+    for (int r = r0 + tid; r < r1; r += kThreads) {
+      float v = 0.f;
+      const float* pp = p.partial + r;
+      for (int ss0 = 0; ss0 < sh.S; ss0 += 8) {
+        float t[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) t[k] = (ss0 + k < sh.S) ? __ldcg(pp + (size_t)(ss0 + k) * sh.m4) : 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (ss0 + k < sh.S) v += t[k];
+      }
+      if (p.yf) p.yf[r] = v;
+      else p.y[r] = __float2half_rn(v);
+    }
+    __syncthreads();
+    if (tid == 0 && atomicAdd(depart, 1u) == (unsigned)sh.S - 1) {  // the last one resets the pair
+      *arrive = 0u;
+      *depart = 0u;
+    }
+  }
+  pdl_launch_dependents();  // the next kernel may now be scheduled
 }
 
 // ---------------------------------------------------------------------------
@@ -506,8 +556,6 @@ __global__ void __launch_bounds__(256) lut_reduce_kernel(const float* __restrict
                                                          unsigned* __restrict__ counters) {
   pdl_launch_dependents();  // the next product may start streaming its weights
   pdl_wait();               // partials are complete and visible
-  if (blockIdx.x == 0)
-    for (int t = threadIdx.x; t < S; t += blockDim.x) counters[t] = 0u;  // chunk counters for the next launch
   const int RQ = m4 / 4;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= b * RQ) return;
@@ -574,7 +622,7 @@ static cudaError_t launch(K kernel, int grid, const KParams& p, cudaStream_t st)
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = st;
   cfg.attrs = &g_pdl_attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = p.xmode == 3 ? 0 : 1;  // experiment 3: no PDL
   return cudaLaunchKernelEx(&cfg, kernel, p);
 }
 
@@ -592,7 +640,7 @@ static cudaError_t launch_reduce(const KParams& p, cudaStream_t st) {
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
   cfg.attrs = &g_pdl_attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = p.xmode == 3 ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, lut_reduce_kernel, (const float*)p.partial, p.sh.S, p.b, p.sh.m, p.sh.m4, p.y,
                             p.yf, p.counters);
 }
@@ -600,7 +648,7 @@ static cudaError_t launch_reduce(const KParams& p, cudaStream_t st) {
 template <int QT, bool HAS_Z>
 static cudaError_t launch_gemv_t(const KParams& p, int grid, cudaStream_t st) {
   // quads in flight per warp while one is computed (ring of PD + 1 buffers)
-  constexpr int PD = QT <= 2 ? 3 : (QT <= 4 ? 2 : 1);
+  constexpr int PD = QT <= 1 ? 6 : (QT <= 2 ? 4 : (QT <= 4 ? 2 : 1));
   if constexpr (QT == 3 && !HAS_Z) {
     if (p.xmode >= 10) {  // measurement variants (LUTGEMM_XMODE)
     switch (p.xmode) {
@@ -634,7 +682,7 @@ static cudaError_t dispatch_q(const KParams& p, int grid, cudaStream_t st, bool 
   }
 }
 
-static size_t counters_bytes(const Shape& sh) { return ((size_t)sh.S * 4u + 255) / 256 * 256; }
+static size_t counters_bytes(const Shape&) { return 2u * kFusedMaxJ * 4u; }
 
 size_t workspace_bytes(const Shape& sh, int b) {
   return counters_bytes(sh) + ((size_t)sh.S * (size_t)b * (size_t)sh.m4 * 4u + 255) / 256 * 256;
@@ -692,9 +740,22 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
     const int rbq = kWarps * kQPW;
     p.items = (long long)sh.S * ((sh.RQ + rbq - 1) / rbq);
   }
-  const int grid = (int)std::min<long long>((long long)num_sms(), p.items);
+  int grid = (int)std::min<long long>((long long)num_sms(), p.items);
+  // fused mode (b = 1): whole slices per CTA group, S*J CTAs with J per slice,
+  // when that idles at most 8 % of the SMs; the reduction then runs in-kernel
+  p.fused_J = 0;
+  if (!batched && p.xmode != 4) {
+    const int sms = num_sms();
+    const int J = sh.S <= sms ? sms / sh.S : 0;
+    if (J >= 1 && J <= kFusedMaxJ && sh.S * J * 100 >= sms * 92 && sh.RQ >= J) {
+      p.fused_J = J;
+      grid = sh.S * J;
+    }
+  }
   cudaError_t e = sh.has_z ? dispatch_q<true>(p, grid, st, batched) : dispatch_q<false>(p, grid, st, batched);
   if (e != cudaSuccess) return e;
+  if (p.fused_J > 0) return cudaSuccess;  // reduced in-kernel
+  if (p.xmode == 2) return cudaSuccess;  // experiment: no reduction (wrong results, timing only)
   return launch_reduce(p, st);
 }
 

@@ -45,10 +45,10 @@ def test_abi_version_and_sizes():
     assert L.lutgemm_packed_bytes(22013, 8192, 4, 128, True) == 22016 * 4 * 1024 + 22016 * 64 * 4 * 2 + 22016 * 64 * 2
     # row-wise g > 1024: the group's scales repeat in each of the S slices; regions 256-B padded
     assert L.lutgemm_packed_bytes(8, 2048, 3, 2048, False) == 2 * (2 * 1536 + 256)
-    # workspace: S chunk counters (256-B rounded) + S*b*m4 fp32 split-K partials (256-B rounded)
-    assert L.lutgemm_workspace_bytes(49152, 12288, 1) == 256 + 12 * 49152 * 4
-    assert L.lutgemm_workspace_bytes(49152, 12288, 4) == 256 + 12 * 4 * 49152 * 4
-    assert L.lutgemm_workspace_bytes(5, 1056, 3) == 256 + (2 * 3 * 8 * 4 + 255) // 256 * 256
+    # workspace: 2 x 256 u32 group counters + S*b*m4 fp32 split-K partials (256-B rounded)
+    assert L.lutgemm_workspace_bytes(49152, 12288, 1) == 2048 + 12 * 49152 * 4
+    assert L.lutgemm_workspace_bytes(49152, 12288, 4) == 2048 + 12 * 4 * 49152 * 4
+    assert L.lutgemm_workspace_bytes(5, 1056, 3) == 2048 + (2 * 3 * 8 * 4 + 255) // 256 * 256
 
 
 @pytest.mark.parametrize("m,n,q,g", [(0, 64, 3, 32), (8, 48, 3, 48), (8, 64, 0, 32), (8, 64, 9, 32),

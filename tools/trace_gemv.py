@@ -15,9 +15,13 @@ from workloads import CONFIGS, gen_bcq, gen_x  # noqa: E402
 
 
 def main(name="fc1", reps=3):
-    c = CONFIGS[name]
-    m, n, q, g = c["m"], c["n"], c["q"], c["g"]
-    d = gen_bcq(c["seed"], m, n, q, g)
+    if name in CONFIGS:
+        c = CONFIGS[name]
+        m, n, q, g, seed = c["m"], c["n"], c["q"], c["g"], c["seed"]
+    else:  # "m,n,q,g"
+        m, n, q, g = (int(v) for v in name.split(","))
+        seed = 5
+    d = gen_bcq(seed, m, n, q, g)
     ws_ = [L.lutgemm_pack_bcq(torch.from_numpy(d["planes"].view(np.int32)).cuda(), torch.from_numpy(d["alpha"]).cuda(),
                               None, n, g) for _ in range(2)]
     x = torch.from_numpy(gen_x(1, 1, n)[0]).cuda()
