@@ -47,7 +47,7 @@ namespace lg {
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-constexpr int kQPW = 8;                // batched: row quads per warp per work item
+constexpr int kQPW = 9;                // batched: row quads per warp per work item (multiple of the ring size)
 constexpr int kMiscBytes = 8192;       // x double buffer (2 x 2 KB) + mbarriers + flags
 constexpr int kSmemBytes = 3 * 65536;  // LUT (128 KB) on a 64 KB boundary + misc, for any base
 constexpr int kPfSteps = 8;            // GEMV: L2 prefetch distance in 16-quad steps
@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
 // tables hold P = 32/B layout lanes x 4 chunks x B batch rows, so a native
 // slice is processed as B sub-slices with register accumulators across them.
 // ---------------------------------------------------------------------------
-template <int QT, bool HAS_Z, int PD>
+template <int QT, bool HAS_Z, int PD, int QPW>
 __global__ void __launch_bounds__(kThreads, 1) lut_gemm_batched_kernel(const KParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31;
@@ -449,86 +449,105 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemm_batched_kernel(const KPa
   const int q = QT <= 4 ? QT : sh.q;
   const int bl = p.bl, B = 1 << bl, P = 32 >> bl, b = p.b;
   const int beta = lane & (B - 1), pp = lane >> bl;
-  const int rbq = kWarps * kQPW;  // row quads per work item
+  constexpr int NB = PD + 1;  // ring buffers; loads for quad t+PD issued before quad t's lookups
+  static_assert(QPW % NB == 0, "the ring restarts at buffer 0 every sub-slice");
+  const int rbq = kWarps * QPW;  // row quads per work item
   const int NRB = (sh.RQ + rbq - 1) / rbq;
   const long long it0 = p.items * blockIdx.x / gridDim.x;
   const long long it1 = p.items * (blockIdx.x + 1) / gridDim.x;
   if (it0 >= it1) return;
 
   const SmemMap sm = map_smem(smem);
-  __half* xbuf0 = reinterpret_cast<__half*>(sm.misc_p);
-  __half* xbuf1 = reinterpret_cast<__half*>(sm.misc_p + 2048);
-  const uint32_t bar0 = sm.misc + 4096, bar1 = sm.misc + 4104;
+  // two x tiles [B][32P] fp16 (2 KB each), filled by cp.async one sub-slice ahead
+  const __half* xtile0 = reinterpret_cast<const __half*>(sm.misc_p);
+  const __half* xtile1 = reinterpret_cast<const __half*>(sm.misc_p + 2048);
+  const uint32_t xt0 = sm.misc, xt1 = sm.misc + 2048;
   const uint32_t lc = (sm.lut & 0xFFFF0000u) | ((uint32_t)(4 * lane + 128) << 8) | (uint32_t)(4 * lane);
 
-  // the records of item itx (one contiguous range) into L2
-  auto prefetch_item = [&](long long itx) {
+  // x tile of sub-slice (itx, k) -- x[beta][col0 .. col0 + 32P) for every
+  // table bank beta, zero for beta >= b and lanes past the slice end -- one
+  // 16-byte cp.async per thread for the first 128 threads (x is L2-resident)
+  auto load_x = [&](uint32_t dst, long long itx, int k) {
+    if (tid < 128) {
+      const int s = (int)(itx / NRB);
+      const int Ls = slice_lanes(sh.n, s);
+      const int bt = tid / (4 * P), c = tid % (4 * P);  // row of the tile, 16-byte chunk in the row
+      const bool ok = bt < b && k * P + c / 4 < Ls;
+      const __half* src = ok ? p.x + (size_t)bt * sh.n + s * kSliceCols + 32 * k * P + 8 * c : p.x;
+      cp_async_16(dst + 16u * tid, src, ok ? 16u : 0u);
+    }
+  };
+  // the (item, sub-slice) after (itx, k)
+  auto advance = [&](long long& itx, int& k) {
+    const int Ls = slice_lanes(sh.n, (int)(itx / NRB));
+    if (++k >= (Ls + P - 1) / P) {
+      k = 0;
+      ++itx;
+    }
+  };
+  Ring<QT> ring[NB];
+  // first PD quads of sub-slice (itx, k) for this warp into ring[0..PD)
+  auto prologue = [&](long long itx, int k) {
     const int s = (int)(itx / NRB), rb = (int)(itx % NRB);
     const int Ls = slice_lanes(sh.n, s);
-    const int lo = rb * rbq, hi = min(sh.RQ, lo + rbq);
-    prefetch_quads(sh, p.data, s, Ls, lo, hi);
-  };
-  // staging of sub-slice (s, k): P lanes starting at layout lane k*P
-  auto stage = [&](int ebuf, long long itx, int k) {
-    const int s = (int)(itx / NRB);
-    const int Ls = slice_lanes(sh.n, s);
-    const int nl = min(P, Ls - k * P);
-    stage_x((ebuf & 1) ? xbuf1 : xbuf0, (ebuf & 1) ? bar1 : bar0, p.x, sh.n, s * kSliceCols + 32 * k * P, nl, P,
-            min(b, B), B, lane);
+    const int lay = k * P + pp;
+    const bool ok = lay < Ls;
+    const LaneAddr la = lane_addr(sh, p.data, s, Ls, ok ? lay : 0);
+    const int rq_w = rb * rbq + warp * QPW;
+#pragma unroll
+    for (int d = 0; d < PD; ++d) ring_load<QT, HAS_Z>(ring[d], ok && rq_w + d < sh.RQ, la, rq_w + d, q);
   };
 
-  if (tid == 0) {
-    mbar_init(bar0, 1);
-    mbar_init(bar1, 1);
-    fence_mbar_init();
-    prefetch_item(it0);
-  }
-  pdl_wait();  // x and the workspace belong to the preceding kernel until it completes
+  prologue(it0, 0);  // weights only: legal before the PDL wait
+  pdl_wait();        // x and the workspace belong to the preceding kernel until it completes
+  load_x(xt0, it0, 0);
+  cp_async_wait_all();
   __syncthreads();
-  if (warp == 0) stage(0, it0, 0);
-  __syncthreads();
+  int e = 0;  // sub-slices processed: x tile e & 1
 
-  int e = 0;
   for (long long it = it0; it < it1; ++it) {
     const int s = (int)(it / NRB);
     const int rb = (int)(it % NRB);
     const int Ls = slice_lanes(sh.n, s);
     const int nsub = (Ls + P - 1) / P;
-    const int rq_w = rb * rbq + warp * kQPW;  // this warp's first quad
-    if (tid == 0 && it + 1 < it1) prefetch_item(it + 1);
-    f32x2 acc01[kQPW], acc23[kQPW];
+    const int rq_w = rb * rbq + warp * QPW;  // this warp's first quad
+    f32x2 acc01[QPW], acc23[QPW];
 
     for (int k = 0; k < nsub; ++k, ++e) {
+      unsigned long long* tr = (p.trace && tid == 0 && it == it0 && k >= 2 && k < 4)
+                                   ? p.trace + (size_t)blockIdx.x * kTraceSlots + 4 * (k - 2) : nullptr;
+      if (tr) tr[0] = globaltimer_ns();
       const int lay = k * P + pp;
       const bool lane_ok = lay < Ls;
       const LaneAddr la = lane_addr(sh, p.data, s, Ls, lane_ok ? lay : 0);
-      Ring<QT> ring[PD];
-#pragma unroll
-      for (int d = 0; d < PD; ++d) ring_load<QT, HAS_Z>(ring[d], lane_ok && rq_w + d < sh.RQ, la, rq_w + d, q);
-      __half* xb = (e & 1) ? xbuf1 : xbuf0;
-      mbar_wait((e & 1) ? bar1 : bar0, (uint32_t)((e >> 1) & 1));
+      if (tr) tr[1] = globaltimer_ns();
       {
         const int l = lane, j = warp & 3, h = warp >> 2;
         const int bt = l & (B - 1), pl = l >> bl;
-        build_table_part(sm.lut + table_offset(l, j), xb + (size_t)bt * 32 * P + (4 * pl + j) * 8, h);
+        build_table_part(sm.lut + table_offset(l, j), ((e & 1) ? xtile1 : xtile0) + (size_t)bt * 32 * P + (4 * pl + j) * 8,
+                         h);
       }
       __syncthreads();
-      if (warp == 0) {
-        if (k + 1 < nsub) stage(e + 1, it, k + 1);
-        else if (it + 1 < it1) stage(e + 1, it + 1, 0);
-      }
+      if (tr) tr[2] = globaltimer_ns();
+      long long itn = it;
+      int kn = k;
+      advance(itn, kn);
+      if (itn < it1) load_x((e & 1) ? xt0 : xt1, itn, kn);  // lands during the lookups
       const float xsum = (HAS_Z && lane_ok) ? lane_xsum(sm.lut, lane) : 0.f;
 #pragma unroll
-      for (int t = 0; t < kQPW; ++t) {
-        const int d = t % PD;
-        ring_compute<QT, HAS_Z>(ring[d], lc, xsum, acc01[t], acc23[t], q, k > 0);
-        if (t + PD < kQPW) ring_load<QT, HAS_Z>(ring[d], lane_ok && rq_w + t + PD < sh.RQ, la, rq_w + t + PD, q);
+      for (int t = 0; t < QPW; ++t) {
+        if (t + PD < QPW)
+          ring_load<QT, HAS_Z>(ring[(t + PD) % NB], lane_ok && rq_w + t + PD < sh.RQ, la, rq_w + t + PD, q);
+        ring_compute<QT, HAS_Z>(ring[t % NB], lc, xsum, acc01[t], acc23[t], q, k > 0);
       }
-      __syncthreads();  // LUT is rebuilt next
+      if (itn < it1) prologue(itn, kn);  // next sub-slice's first quads fly during the barrier and rebuild
+      if (tr) tr[3] = globaltimer_ns();
+      cp_async_wait_all();
+      __syncthreads();  // every warp is done with the LUT; the next x tile is visible
     }
     // reduce over the P layout lanes that share a batch row (lane bits >= bl)
 #pragma unroll
-    for (int t = 0; t < kQPW; ++t) {
+    for (int t = 0; t < QPW; ++t) {
       float2 v01 = unpack2(acc01[t]), v23 = unpack2(acc23[t]);
       for (int off = 16; off >= B; off >>= 1) {
         v01.x += __shfl_xor_sync(kFull, v01.x, off);
@@ -665,10 +684,16 @@ static cudaError_t launch_gemv_t(const KParams& p, int grid, cudaStream_t st) {
   return launch(lut_gemv_kernel<QT, HAS_Z, PD>, grid, p, st);
 }
 
+static int batched_qpw(const KParams& p) { return p.xmode == 6 ? 6 : (p.xmode == 7 ? 8 : kQPW); }
+
 template <int QT, bool HAS_Z>
 static cudaError_t launch_batched_t(const KParams& p, int grid, cudaStream_t st) {
-  constexpr int PD = QT <= 2 ? 4 : (QT <= 4 ? 2 : 1);
-  return launch(lut_gemm_batched_kernel<QT, HAS_Z, PD>, grid, p, st);
+  constexpr int PD = QT <= 4 ? 2 : 0;  // QPW % (PD + 1) == 0
+  if constexpr (QT <= 4) {
+    if (p.xmode == 6) return launch(lut_gemm_batched_kernel<QT, HAS_Z, PD, 6>, grid, p, st);
+    if (p.xmode == 7) return launch(lut_gemm_batched_kernel<QT, HAS_Z, 1, 8>, grid, p, st);
+  }
+  return launch(lut_gemm_batched_kernel<QT, HAS_Z, PD, kQPW>, grid, p, st);
 }
 
 template <bool HAS_Z>
@@ -737,7 +762,7 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
   if (!batched) {
     p.items = (long long)sh.S * sh.RQ;
   } else {
-    const int rbq = kWarps * kQPW;
+    const int rbq = kWarps * batched_qpw(p);
     p.items = (long long)sh.S * ((sh.RQ + rbq - 1) / rbq);
   }
   int grid = (int)std::min<long long>((long long)num_sms(), p.items);

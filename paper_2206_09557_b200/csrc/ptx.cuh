@@ -51,6 +51,12 @@ __device__ __forceinline__ uint2 ldg_nc_u2(const void* p) {
   return r;
 }
 
+// 16-byte async global->shared copy (LDGSTS); src_bytes = 0 writes zeros
+__device__ __forceinline__ void cp_async_16(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // ---- mbarrier + bulk async copy (TMA engine, SASS UBLKCP) ----
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
