@@ -1,0 +1,194 @@
+"""BASELINE config 5: the full OPT-175B decoder linear stack (96 layers x
+{QKV 36864x12288, out 12288x12288, fc1 49152x12288, fc2 12288x49152}, q=3,
+g=128), one token (b=1), per-token latency on 1 GPU or tensor-parallel.
+
+    python tools/stack.py [--layers 96] [--tokens 20] [--check]
+    torchrun --nproc-per-node P tools/stack.py ...
+
+Tensor parallelism (Megatron pairing): QKV and fc1 are split by
+rows (no communication), out-proj and fc2 by columns -- each rank's input is
+its own QKV / fc1 output slice -- followed by an fp32 all-reduce of y
+(lutgemm_tp_linear COLS_ALLREDUCE): 2 all-reduces per layer.  Attention, LN
+and embeddings are omitted (the path is the linears): out-proj reads the first
+12288/P outputs of QKV.  Weights are seeded synthetic BCQ (device RNG), 73.4 GB
+at P=1.  One token = one CUDA graph of 384 LUT-GEMMs (+ 192 all-reduces).
+
+--check: for layers 0 and L-1 each linear is also run on a seeded x and 64
+sampled rows are compared with the fp64 oracle (its inputs are the seeded
+canonical weights copied to the host before packing, never a CUDA output).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2206_09557_b200 as L  # noqa: E402
+
+H = 12288
+LINEARS = [("qkv", 3 * H, H, "rows"), ("out", H, H, "cols"), ("fc1", 4 * H, H, "rows"), ("fc2", H, 4 * H, "cols")]
+Q, G = 3, 128
+
+
+def gen_canonical(seed: int, m: int, n: int, dev):
+    """Device-generated canonical BCQ (same distributions as workloads.gen_bcq)."""
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed)
+    planes = torch.randint(0, 256, (Q, m, n // 32 * 4), dtype=torch.uint8, device=dev, generator=gen)
+    planes = planes.view(torch.int32)
+    u = torch.rand((m, n // G, Q), device=dev, generator=gen) * 0.5 + 0.75
+    alpha = (0.87 * (2.0 ** -torch.arange(Q, device=dev)) * u / math.sqrt(n)).to(torch.float16)
+    return planes.contiguous(), alpha.contiguous()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--layers", type=int, default=96)
+    ap.add_argument("--tokens", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--check", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        comm = L.TPComm(rank, world, device=dev)
+
+    t0 = time.time()
+    weights = []  # per layer: dict name -> PackedBCQ
+    check_rows = {}
+    rng = np.random.default_rng(0)
+    for layer in range(args.layers):
+        lw = {}
+        for li, (name, m, n, split) in enumerate(LINEARS):
+            ms, ns = (m // world, n) if split == "rows" else (m, n // world)
+            seed = 1_000_003 * layer + 1009 * li + rank
+            planes, alpha = gen_canonical(seed, ms, ns, dev)
+            if args.check and layer in (0, args.layers - 1):
+                rows = np.sort(rng.choice(ms, size=64, replace=False))
+                idx = torch.from_numpy(rows).to(dev)
+                check_rows[(layer, name)] = (rows, planes[:, idx].cpu().numpy().view(np.uint32),
+                                             alpha[idx].cpu().numpy(), ms, ns)
+            lw[name] = L.lutgemm_pack_bcq(planes, alpha, None, ns, G)
+            del planes, alpha
+        weights.append(lw)
+    torch.cuda.synchronize()
+    build_s = time.time() - t0
+    mem_gb = torch.cuda.memory_allocated(dev) / 1e9
+
+    # activations (each rank: full x; local QKV/fc1 outputs; replicated out/fc2 outputs)
+    x0 = torch.randn(H, device=dev).to(torch.float16)
+    x = x0.clone()
+    qkv_o = torch.empty(3 * H // world, dtype=torch.float16, device=dev)
+    out_o = torch.empty(H, dtype=torch.float16, device=dev)
+    fc1_o = torch.empty(4 * H // world, dtype=torch.float16, device=dev)
+    ws_bytes = max(L.lutgemm_workspace_bytes(m // world if s == "rows" else m, n if s == "rows" else n // world, 1)
+                   for _, m, n, s in LINEARS)
+    ws = L.make_workspace(ws_bytes, dev)
+    tws = None
+    if comm is not None:
+        tws = L.make_workspace(max(comm.workspace_bytes(L.TP_COLS_ALLREDUCE, H, H // world, 1),
+                                   comm.workspace_bytes(L.TP_COLS_ALLREDUCE, H, 4 * H // world, 1)), dev)
+
+    def cols(w, xin, y):
+        if comm is None:
+            L.lutgemm_gemv(w, xin, y, ws)
+        else:
+            comm.linear(L.TP_COLS_ALLREDUCE, w, xin, y, tws)
+
+    def token():
+        x.copy_(x0)  # every token starts from the same input (device-to-device copy)
+        for lw in weights:
+            L.lutgemm_gemv(lw["qkv"], x, qkv_o, ws)
+            cols(lw["out"], qkv_o[:H // world], out_o)
+            L.lutgemm_gemv(lw["fc1"], out_o, fc1_o, ws)
+            cols(lw["fc2"], fc1_o, x)
+
+    token()
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream()
+    cap.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.graph(graph, stream=cap):
+        token()
+    for _ in range(args.warmup):
+        graph.replay()
+    torch.cuda.synchronize()
+    if comm is not None:
+        torch.distributed.barrier(device_ids=[local])
+    a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.tokens):
+        graph.replay()
+    e.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(e) / args.tokens
+    if comm is not None:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t[0])
+    finite = bool(torch.isfinite(x.float()).all())
+
+    # per-linear breakdown on this rank (eager, events around each call of one layer)
+    per = {}
+    for name in ("qkv", "out", "fc1", "fc2"):
+        lw = weights[args.layers // 2]
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        xin, y = {"qkv": (x, qkv_o), "out": (qkv_o[:H // world], out_o), "fc1": (out_o, fc1_o),
+                  "fc2": (fc1_o, x)}[name]
+        for _ in range(3):
+            (L.lutgemm_gemv(lw[name], xin, y, ws) if name in ("qkv", "fc1") else cols(lw[name], xin, y))
+        torch.cuda.synchronize()
+        ev0.record()
+        for _ in range(20):
+            (L.lutgemm_gemv(lw[name], xin, y, ws) if name in ("qkv", "fc1") else cols(lw[name], xin, y))
+        ev1.record()
+        torch.cuda.synchronize()
+        per[name] = round(ev0.elapsed_time(ev1) / 20 * 1e3, 2)
+
+    # parity on layers 0 and L-1 with a seeded x (oracle inputs never come from the GPU)
+    parity = {}
+    if args.check:
+        import oracle as O
+        for (layer, name), (rows, planes_rows, alpha_rows, ms_, ns_) in sorted(check_rows.items()):
+            xs = np.random.default_rng(layer * 7 + len(name)).standard_normal(ns_).astype(np.float16)
+            y = torch.empty(ms_, dtype=torch.float16, device=dev)
+            L.lutgemm_gemv(weights[layer][name], torch.from_numpy(xs).to(dev), y, ws)
+            torch.cuda.synchronize()
+            got = y.float().cpu().numpy()[rows].astype(np.float64)
+            ref = O.bcq_gemv(planes_rows, alpha_rows, None, xs[None], ns_, G)[0]
+            parity[f"L{layer}.{name}"] = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+
+    bytes_token = sum(((m // world) * n if s == "rows" else m * (n // world)) * (Q / 8 + 2 * Q / G)
+                      for _, m, n, s in LINEARS) * args.layers
+    if rank == 0:
+        print(json.dumps({
+            "config": "OPT-175B decoder linear stack (96 x QKV/out/fc1/fc2), q=3 g=128, b=1",
+            "layers": args.layers, "tp": world, "ms_per_token": round(ms, 4),
+            "GBps_per_gpu": round(bytes_token / (ms * 1e-3) / 1e9, 1),
+            "weight_bytes_per_gpu": int(bytes_token), "allreduces_per_token": 2 * args.layers if world > 1 else 0,
+            "per_linear_us_eager": per, "finite": finite, "build_s": round(build_s, 1),
+            "hbm_alloc_gb": round(mem_gb, 1), "parity_rel_l2_sampled": parity,
+            "paper_context_ms": "A100 FT e2e per token, 3-bit row-wise: 51.6 (1 GPU), 35.8 (2), 27.2 (4), 24.2 (8) (Table 4 P:L475-478)",
+        }), flush=True)
+    if comm is not None:
+        comm.close()
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
