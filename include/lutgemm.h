@@ -158,7 +158,7 @@ size_t lutgemm_host_workspace_bytes(int m, int n, int b);
 lutgemm_status lutgemm_gemm_host(const lutgemm_weight* w, const uint16_t* X_host, int b, uint16_t* Y_host,
                                  void* ws, size_t ws_bytes, void* stream);
 
-/* Tracing (debug; not for the hot path).  When enabled, every subsequent
+/* Tracing (debug; not for the hot path).  Enabling clears the buffer; then every subsequent
  * product launch records a per-CTA %globaltimer timeline into a library-owned
  * device buffer (8 u64 per CTA, up to 1024 CTAs, last launch wins):
  * [0] CTA start, [1] x slice staged, [2] first LUT built, [3] warp 0 done with

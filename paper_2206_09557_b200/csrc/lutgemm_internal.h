@@ -21,6 +21,7 @@ struct KParams {
   int b;
   int bl;            // log2 of the table-bank count B >= b
   int pf_steps;      // GEMV: L2 prefetch distance in 16-quad steps
+  int pf_init;       // GEMV: 16-quad steps bulk-prefetched into L2 before the PDL wait
   int xmode;         // experiment knob (0 default)
   int fused_J;       // GEMV: CTAs per slice in the fused-reduction mode (0: separate reduction kernel)
   long long items;

@@ -330,11 +330,15 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     //    else, so it is not queued behind the weight stream; then an L2
     //    prefetch of the first weight steps and the register ring
     if (e == 0) {
+      // weights of the steps after the register prologue into L2 while the
+      // preceding kernel drains (a plain prefetch: legal before the PDL wait)
+      if (tid == 0 && p.pf_init > PD)
+        prefetch_quads(sh, p.data, s, Ls, min(rq_b, rq_a + PD * kWarps), min(rq_b, rq_a + p.pf_init * kWarps));
       pdl_wait();
       if (trace) trace[5] = globaltimer_ns();
       if (warp == 0) stage_x(xbuf0, bar0, p.x, sh.n, s * kSliceCols, Ls, 32, 1, 1, lane);
     }
-    if (tid == 0) prefetch_quads(sh, p.data, s, Ls, rq_a, min(rq_b, rq_a + pf_steps * kWarps));
+    if (tid == 0 && pf_steps > 0) prefetch_quads(sh, p.data, s, Ls, rq_a, min(rq_b, rq_a + pf_steps * kWarps));
     // this warp's row quads in the segment: rq_a + warp + 16 t, t < nt
     const int nt = rq_a + warp < rq_b ? (rq_b - (rq_a + warp) + kWarps - 1) / kWarps : 0;
     // a ring of NB = PD + 1 single-quad buffers: the load for quad t + PD is
@@ -720,10 +724,8 @@ constexpr int kTraceMaxCtas = 1024;
 
 void trace_enable(int on) {
   g_trace_on = on != 0;
-  if (g_trace_on && !g_trace) {
-    cudaMalloc(&g_trace, sizeof(unsigned long long) * kTraceSlots * kTraceMaxCtas);
-    cudaMemset(g_trace, 0, sizeof(unsigned long long) * kTraceSlots * kTraceMaxCtas);
-  }
+  if (g_trace_on && !g_trace) cudaMalloc(&g_trace, sizeof(unsigned long long) * kTraceSlots * kTraceMaxCtas);
+  if (g_trace_on && g_trace) cudaMemset(g_trace, 0, sizeof(unsigned long long) * kTraceSlots * kTraceMaxCtas);
 }
 
 size_t trace_read(unsigned long long* host, size_t n) {
@@ -754,6 +756,14 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
   p.bl = bl;
   p.pf_steps = g_pf_steps;
   {
+    static int pf_init = -1;
+    if (pf_init < 0) {
+      const char* env = getenv("LUTGEMM_PF_INIT");  // tuning knob
+      pf_init = env ? atoi(env) : 0;
+    }
+    p.pf_init = pf_init;
+  }
+  {
     const char* env = getenv("LUTGEMM_XMODE");  // experiment knob
     p.xmode = env ? atoi(env) : 0;
   }
@@ -772,7 +782,7 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
   if (!batched && p.xmode != 4) {
     const int sms = num_sms();
     const int J = sh.S <= sms ? sms / sh.S : 0;
-    if (J >= 1 && J <= kFusedMaxJ && sh.S * J * 100 >= sms * 92 && sh.RQ >= J) {
+    if (J >= 1 && J <= kFusedMaxJ && sh.S <= kFusedMaxJ && sh.S * J * 100 >= sms * 92 && sh.RQ >= J) {
       p.fused_J = J;
       grid = sh.S * J;
     }
