@@ -390,6 +390,10 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
       }
     }
     if (trace && e == 0) trace[3] = globaltimer_ns();  // warp 0's loop end
+    if (J > 0) {  // fused mode: each warp publishes its partials with one release increment
+      __syncwarp();
+      if (lane == 0) red_release_add_u32(p.counters + blockIdx.x % J, 1u);
+    }
     __syncthreads();  // the LUT and x buffer are reused by the next segment
     if (trace) trace[e == 0 ? 4 : 6] = globaltimer_ns();  // all warps done
     it = itn;
@@ -404,26 +408,27 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     const int fs = blockIdx.x / J, fj = blockIdx.x % J;
     unsigned* arrive = p.counters + fj;
     unsigned* depart = p.counters + kFusedMaxJ + fj;
-    if (e == 0) pdl_wait();  // (an empty range never reached the wait above)
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) {
-      atomicAdd(arrive, 1u);
-      while (ld_acquire_u32(arrive) < (unsigned)sh.S) __nanosleep(32);
+    if (e == 0) {  // an empty range never reached the wait and the warp increments above
+      pdl_wait();
+      if (lane == 0) red_release_add_u32(arrive, 1u);
+    }
+    if (tid == 0) {  // all 16 warps of all S CTAs of the group have published their partials
+      while (ld_acquire_u32(arrive) < (unsigned)(sh.S * kWarps)) __nanosleep(32);
     }
     __syncthreads();
+    if (trace) trace[5] = globaltimer_ns();  // (re-used) the group is complete
     const int g0 = (int)((long long)sh.RQ * fj / J), g1 = (int)((long long)sh.RQ * (fj + 1) / J);
     const int r0 = 4 * (g0 + (int)((long long)(g1 - g0) * fs / sh.S));
     const int r1 = min(sh.m, 4 * (g0 + (int)((long long)(g1 - g0) * (fs + 1) / sh.S)));
     for (int r = r0 + tid; r < r1; r += kThreads) {
       float v = 0.f;
       const float* pp = p.partial + r;
-      for (int ss0 = 0; ss0 < sh.S; ss0 += 8) {
-        float t[8];
+      for (int ss0 = 0; ss0 < sh.S; ss0 += 16) {  // up to 16 slices per L2 round trip
+        float t[16];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) t[k] = (ss0 + k < sh.S) ? __ldcg(pp + (size_t)(ss0 + k) * sh.m4) : 0.f;
+        for (int k = 0; k < 16; ++k) t[k] = (ss0 + k < sh.S) ? __ldcg(pp + (size_t)(ss0 + k) * sh.m4) : 0.f;
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
+        for (int k = 0; k < 16; ++k)
           if (ss0 + k < sh.S) v += t[k];
       }
       if (p.yf) p.yf[r] = v;
@@ -434,6 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
       *arrive = 0u;
       *depart = 0u;
     }
+    if (trace) trace[6] = globaltimer_ns();  // reduction share done
   }
   pdl_launch_dependents();  // the next kernel may now be scheduled
 }
@@ -767,7 +773,10 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
     const char* env = getenv("LUTGEMM_XMODE");  // experiment knob
     p.xmode = env ? atoi(env) : 0;
   }
-  p.trace = g_trace_on ? g_trace : nullptr;
+  {
+    static unsigned seq = 0;  // consecutive launches alternate between two halves of the trace buffer
+    p.trace = g_trace_on ? g_trace + (size_t)(seq++ & 1u) * (kTraceMaxCtas / 2) * kTraceSlots : nullptr;
+  }
   const bool batched = b > 1;
   if (!batched) {
     p.items = (long long)sh.S * sh.RQ;
