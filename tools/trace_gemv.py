@@ -34,8 +34,8 @@ def main(name="fc1", reps=3):
         L.lutgemm_trace_enable(True)  # clears nothing: stale CTAs are filtered by a zero start below
         L.lutgemm_gemv(ws_[r % 2], x, y, wsb)
         torch.cuda.synchronize()
-        t = L.lutgemm_trace_read(148).astype(np.int64)
-        t = t[t[:, 0] > 0]
+        t = L.lutgemm_trace_read(1024).astype(np.int64)
+        t = np.concatenate([t[:512][t[:512, 0] > 0], t[512:][t[512:, 0] > 0]])
         nsl = t[:, 7] >> 32
         t[:, 7] &= 0xFFFFFFFF
         t0 = t[:, 0].min()
