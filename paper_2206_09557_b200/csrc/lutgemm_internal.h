@@ -19,7 +19,11 @@ struct KParams {
   unsigned* counters;  // GEMV fused mode: arrive/depart counters per row-quad group (zero between launches)
   Shape sh;
   int b;
-  int bl;            // log2 of the table-bank count B >= b
+  int bl;            // batched: log2 of the padded batch b_pad >= b (partials are [S2][m4][b_pad])
+  int nv;            // batched: V-wide batch vectors per table entry slot group (b_pad = V * nv)
+  int spi;           // batched: LUT slices per work item (split-K factor S2 = ceil(S / spi))
+  int qpw;           // batched: row quads per warp per work item
+  int gsh;           // batched: layout lane -> slice-local group shift (31: one group per slice)
   int pf_steps;      // GEMV: L2 prefetch distance in 16-quad steps
   int pf_init;       // GEMV: 16-quad steps bulk-prefetched into L2 before the PDL wait
   int xmode;         // experiment knob (0 default)
@@ -34,6 +38,8 @@ void trace_enable(int on);
 size_t trace_read(unsigned long long* host, size_t n);
 
 size_t workspace_bytes(const Shape& sh, int b);
+// padded batch of the batched kernel's partials (1 for the GEMV)
+int batch_pad(int b);
 
 // y (fp16) or yf (fp32) [b][m] = X [b][n] W^T.  Two launches chained with
 // programmatic dependent launch: the LUT kernel (split-K partials), then the

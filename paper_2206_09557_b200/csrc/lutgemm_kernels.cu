@@ -47,7 +47,8 @@ namespace lg {
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-constexpr int kQPW = 9;                // batched: row quads per warp per work item (multiple of the ring size)
+constexpr int kBThreads = 256;         // batched kernel: 8 warps (255 registers per thread)
+constexpr int kBWarps = kBThreads / 32;
 constexpr int kMiscBytes = 8192;       // x double buffer (2 x 2 KB) + mbarriers + flags
 constexpr int kSmemBytes = 3 * 65536;  // LUT (128 KB) on a 64 KB boundary + misc, for any base
 constexpr int kPfSteps = 8;            // GEMV: L2 prefetch distance in 16-quad steps
@@ -445,134 +446,393 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
 }
 
 // ---------------------------------------------------------------------------
-// Batched LUT-GEMM, 2 <= b <= 32.  B = 2^bl >= b table banks
-// share each key: lane l = (pp = l >> bl, beta = l & (B-1)); a CTA's 128
-// tables hold P = 32/B layout lanes x 4 chunks x B batch rows, so a native
-// slice is processed as B sub-slices with register accumulators across them.
+// Batched LUT-GEMM, 2 <= b <= 32 ("diminishing performance gains
+// as the batch size increases ... memory bandwidth between core and LUTs in
+// the shared memory").  The LUT bytes grow x b and the shared-memory crossbar
+// (128 B/clk/SM) becomes the roof, so every lookup moves a VECTOR of V batch
+// rows: one table slot holds T[key] for V consecutive activation rows, one PRMT
+// forms the address and one LDS.128 (V = 4) or LDS.64 (V = 2, b = 2) returns
+// V lookups.  A 128 KB LUT holds 128 fp32 per key: C chunks x b_pad rows with
+// C * b_pad = 128, so a native slice is processed as sub-slices of NW layout
+// lanes (NW * 32 columns), each a LUT rebuild, with register accumulators
+// across sub-slices and across the spi slices of a work item.
+//
+// Lanes: LR = 32 / V lanes form one LDS phase (8 lanes x 16 B or 16 x 8 B =
+// 128 B); lane = rg * LR + wv, wv = w * NV + v: row group rg (4 / V rows of the
+// row quad), layout lane w of the sub-slice, batch vector v (rows vV..vV+V-1).
+// Slot of (chunk 4w + J, vector v) for key k:
+//     LUT + (J >> 1) * 64 KB + k * 256 + (LR * (J & 1) + wv) * 4V
+// The LR lanes of a phase have distinct wv, hence distinct 4V-byte bank groups
+// whatever their keys: conflict-free by construction, and key -> address is
+// still one PRMT (the key byte lands in bits 8..15 next to a lane constant).
 // ---------------------------------------------------------------------------
-template <int QT, bool HAS_Z, int PD, int QPW>
-__global__ void __launch_bounds__(kThreads, 1) lut_gemm_batched_kernel(const KParams p) {
+
+// V lookups of key byte J of word w, as V/2 packed f32x2
+template <int V, int J>
+__device__ __forceinline__ void vlut(uint32_t w, uint32_t lc, f32x2 (&t)[V / 2]) {
+  constexpr uint32_t kSel = ((J & 1) ? 0x7605u : 0x7604u) | ((uint32_t)J << 4);
+  const uint32_t a = prmt<kSel>(w, lc);
+  if constexpr (V == 4) lds_b64x2<(J >> 1) * 65536>(a, t[0], t[1]);
+  else t[0] = lds_b64<(J >> 1) * 65536>(a);
+}
+
+// sum of the 4 chunk lookups of word w (32 columns) for the lane's V batch rows
+template <int V>
+__device__ __forceinline__ void vword(uint32_t w, uint32_t lc, f32x2 (&s)[V / 2]) {
+  f32x2 t0[V / 2], t1[V / 2], t2[V / 2], t3[V / 2];
+  vlut<V, 0>(w, lc, t0);
+  vlut<V, 1>(w, lc, t1);
+  vlut<V, 2>(w, lc, t2);
+  vlut<V, 3>(w, lc, t3);
+#pragma unroll
+  for (int p = 0; p < V / 2; ++p) s[p] = add2(add2(t0[p], t1[p]), add2(t2[p], t3[p]));
+}
+
+// x tile of a sub-slice in shared memory: 128 16-byte cells (8 columns of one
+// activation row each); cell of (column chunk c = 4w + J4, row bt = vV + u) is
+//     (J4 * V + u) * LR + w * NV + v
+// so the 8 builder lanes of one LDS.128 phase (same J4 and u, distinct (w, v))
+// read 8 distinct cells of one 128-byte line: conflict-free.
+template <int V>
+__device__ __forceinline__ int xcell(int c, int bt, int NV) {
+  constexpr int LR = 32 / V;
+  return ((c & 3) * V + bt % V) * LR + (c >> 2) * NV + bt / V;
+}
+
+// Build the sub-slice LUT: slot (region R, key k, slot s) holds
+// T_c[k] for rows vV..vV+V-1 of chunk c = 4w + 2R + s / LR, with (w, v) from
+// wv = s % LR.  T[k] = H(k >> 4) + (+-x0 +- x1) + (+-x2 +- x3): with
+// A1 = x0 - x1, A3 = x0 + x1 the low pair takes -A3, A1, -A1, A3 (likewise B
+// over x2, x3), so each entry costs one packed add after 4 adds per (h, pair).
+template <int V>
+__device__ __forceinline__ void build_vtables(uint32_t lut, const __half* tile, int NV, int tid) {
+  constexpr int LR = 32 / V, NP = V / 2;
+  constexpr int SPR = 2 * LR;                      // slots per region and key
+  constexpr int TPR = kBThreads / 2;               // threads per region
+  constexpr int HPT = 16 * SPR / TPR;              // high nibbles per thread
+  const int R = tid / TPR, rem = tid % TPR;
+  const int s = rem % SPR, h0 = rem / SPR;
+  const int Jp = s / LR, wv = s % LR, w = wv / NV, v = wv % NV;
+  const int c = 4 * w + 2 * R + Jp;
+  f32x2 A1[NP], A3[NP], B1[NP], B3[NP], X4[NP], X5[NP], X6[NP], X7[NP];
+#pragma unroll
+  for (int pp = 0; pp < NP; ++pp) {
+    float x[2][8];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(tile + 8 * xcell<V>(c, v * V + 2 * pp + e, NV));
+      const float2 a = h2_to_f2(raw.x), b = h2_to_f2(raw.y), cc = h2_to_f2(raw.z), d = h2_to_f2(raw.w);
+      x[e][0] = a.x; x[e][1] = a.y; x[e][2] = b.x; x[e][3] = b.y;
+      x[e][4] = cc.x; x[e][5] = cc.y; x[e][6] = d.x; x[e][7] = d.y;
+    }
+    const f32x2 x0 = pack2(x[0][0], x[1][0]), x1 = pack2(x[0][1], x[1][1]);
+    const f32x2 x2 = pack2(x[0][2], x[1][2]), x3 = pack2(x[0][3], x[1][3]);
+    A1[pp] = sub2(x0, x1); A3[pp] = add2(x0, x1);
+    B1[pp] = sub2(x2, x3); B3[pp] = add2(x2, x3);
+    X4[pp] = pack2(x[0][4], x[1][4]); X5[pp] = pack2(x[0][5], x[1][5]);
+    X6[pp] = pack2(x[0][6], x[1][6]); X7[pp] = pack2(x[0][7], x[1][7]);
+  }
+#pragma unroll
+  for (int hh = 0; hh < HPT; ++hh) {
+    const int h = h0 + hh * (16 / HPT);  // key bits 4..7
+    const float g4 = (h & 1) ? 1.f : -1.f, g5 = (h & 2) ? 1.f : -1.f;
+    const float g6 = (h & 4) ? 1.f : -1.f, g7 = (h & 8) ? 1.f : -1.f;
+    f32x2 HA[4][NP];
+#pragma unroll
+    for (int pp = 0; pp < NP; ++pp) {
+      const f32x2 H = fma2(pack2(g4, g4), X4[pp], fma2(pack2(g5, g5), X5[pp],
+                           fma2(pack2(g6, g6), X6[pp], mul2(pack2(g7, g7), X7[pp]))));
+      HA[0][pp] = sub2(H, A3[pp]);
+      HA[1][pp] = add2(H, A1[pp]);
+      HA[2][pp] = sub2(H, A1[pp]);
+      HA[3][pp] = add2(H, A3[pp]);
+    }
+    const uint32_t base = lut + (uint32_t)R * 65536u + (uint32_t)(16 * h) * 256u + (uint32_t)s * (4u * V);
+#pragma unroll
+    for (int lo = 0; lo < 16; ++lo) {
+      f32x2 e[NP];
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp) {
+        const int k2 = lo >> 2;
+        const f32x2 ha = HA[lo & 3][pp];
+        e[pp] = k2 == 0 ? sub2(ha, B3[pp]) : (k2 == 1 ? add2(ha, B1[pp]) : (k2 == 2 ? sub2(ha, B1[pp]) : add2(ha, B3[pp])));
+      }
+      if constexpr (V == 4) sts_b64x2(base + lo * 256u, e[0], e[1]);
+      else sts_b64(base + lo * 256u, e[0]);
+    }
+  }
+}
+
+// One row quad's operands for one lane: the key words of its 4/V rows for q
+// planes, their scales (one fp16 per row, packed) per plane, and z.
+template <int QT, int RPL>
+struct VRing {
+  uint32_t k[QT][RPL];
+  uint32_t a[QT];
+  uint32_t z;
+};
+
+// The lane's running pointers into the three regions of one slice: plane i's
+// key word(s) of the next quad at kq + i * kstride, its scales at aq + 8 i,
+// its z at zq; each advances by the region's per-quad stride.
+struct VPtr {
+  const uint8_t *kq, *aq, *zq;
+  uint32_t KB, AB, ZB, kstride;
+};
+
+template <int QT, int RPL, bool HAS_Z>
+__device__ __forceinline__ void vring_load(VRing<QT, RPL>& r, bool ok, VPtr& pt, int q) {
+#pragma unroll
+  for (int i = 0; i < QT; ++i) {
+    if (QT <= 4 || i < q) {
+      if (ok) {
+        const uint8_t* kp = pt.kq + i * pt.kstride;
+        if constexpr (RPL == 1) {
+          r.k[i][0] = ldg_nc_u32(kp);
+          r.a[i] = ldg_nc_u16(pt.aq + 8 * i);
+        } else {
+          const uint2 kk = ldg_nc_u2(kp);
+          r.k[i][0] = kk.x;
+          r.k[i][1] = kk.y;
+          r.a[i] = ldg_nc_u32(pt.aq + 8 * i);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) r.k[i][u] = 0u;
+        r.a[i] = 0u;
+      }
+    }
+  }
+  if (HAS_Z) r.z = ok ? (RPL == 1 ? ldg_nc_u16(pt.zq) : ldg_nc_u32(pt.zq)) : 0u;
+  pt.kq += pt.KB;
+  pt.aq += pt.AB;
+  if (HAS_Z) pt.zq += pt.ZB;
+}
+
+// acc[rho][p] (+)= sum_i alpha_i[rho] * (word lookups of row rho, plane i) + z[rho] * xsum
+template <int V, int QT, bool HAS_Z>
+__device__ __forceinline__ void vring_compute(const VRing<QT, 4 / V>& r, uint32_t lc, const f32x2 (&xs)[V / 2],
+                                              f32x2 (&acc)[4 / V][V / 2], int q) {
+  constexpr int RPL = 4 / V, NP = V / 2;
+#pragma unroll
+  for (int i = 0; i < QT; ++i) {
+    if (QT <= 4 || i < q) {
+      const float2 af = h2_to_f2(r.a[i]);  // RPL == 1: only .x is meaningful
+#pragma unroll
+      for (int rho = 0; rho < RPL; ++rho) {
+        f32x2 s[NP];
+        vword<V>(r.k[i][rho], lc, s);
+        const float al = rho == 0 ? af.x : af.y;
+        const f32x2 aa = pack2(al, al);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) acc[rho][p] = fma2(aa, s[p], acc[rho][p]);
+      }
+    }
+  }
+  if (HAS_Z) {
+    const float2 zf = h2_to_f2(r.z);
+#pragma unroll
+    for (int rho = 0; rho < RPL; ++rho) {
+      const float zv = rho == 0 ? zf.x : zf.y;
+      const f32x2 zz = pack2(zv, zv);
+#pragma unroll
+      for (int p = 0; p < NP; ++p) acc[rho][p] = fma2(zz, xs[p], acc[rho][p]);
+    }
+  }
+}
+
+// A step of the work loop: sub-slice k of slice s of work item it.
+struct VStep {
+  int it, s, k;
+  int s_end;  // end of the item's slice range
+  int nsub;   // sub-slices of slice s
+};
+
+template <int V, int QT, bool HAS_Z, int PD, int QPW>
+__global__ void __launch_bounds__(kBThreads, 1) lut_gemm_batched_kernel(const KParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int LR = 32 / V, RPL = 4 / V, NP = V / 2, NB = PD + 1;
+  static_assert(QPW % NB == 0, "the ring restarts at buffer 0 every sub-slice");
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(kFull, tid >> 5, 0);
   const Shape sh = p.sh;
   const int q = QT <= 4 ? QT : sh.q;
-  const int bl = p.bl, B = 1 << bl, P = 32 >> bl, b = p.b;
-  const int beta = lane & (B - 1), pp = lane >> bl;
-  constexpr int NB = PD + 1;  // ring buffers; loads for quad t+PD issued before quad t's lookups
-  static_assert(QPW % NB == 0, "the ring restarts at buffer 0 every sub-slice");
-  const int rbq = kWarps * QPW;  // row quads per work item
+  const int NV = p.nv, NW = LR / NV, bpad = V * NV, b = p.b, spi = p.spi;
+  const int rg = lane / LR, wv = lane % LR, w = wv / NV, v = wv % NV;
+  const int rbq = kBWarps * QPW;  // row quads per work item
   const int NRB = (sh.RQ + rbq - 1) / rbq;
-  const long long it0 = p.items * blockIdx.x / gridDim.x;
-  const long long it1 = p.items * (blockIdx.x + 1) / gridDim.x;
+  const int it0 = (int)(p.items * blockIdx.x / gridDim.x);
+  const int it1 = (int)(p.items * (blockIdx.x + 1) / gridDim.x);
   if (it0 >= it1) return;
 
   const SmemMap sm = map_smem(smem);
-  // two x tiles [B][32P] fp16 (2 KB each), filled by cp.async one sub-slice ahead
   const __half* xtile0 = reinterpret_cast<const __half*>(sm.misc_p);
   const __half* xtile1 = reinterpret_cast<const __half*>(sm.misc_p + 2048);
   const uint32_t xt0 = sm.misc, xt1 = sm.misc + 2048;
-  const uint32_t lc = (sm.lut & 0xFFFF0000u) | ((uint32_t)(4 * lane + 128) << 8) | (uint32_t)(4 * lane);
+  const uint32_t lc = (sm.lut & 0xFFFF0000u) | ((uint32_t)((LR + wv) * 4 * V) << 8) | (uint32_t)(wv * 4 * V);
+  const int gsh = p.gsh;  // layout lane p's group in the slice = p >> gsh
 
-  // x tile of sub-slice (itx, k) -- x[beta][col0 .. col0 + 32P) for every
-  // table bank beta, zero for beta >= b and lanes past the slice end -- one
-  // 16-byte cp.async per thread for the first 128 threads (x is L2-resident)
-  auto load_x = [&](uint32_t dst, long long itx, int k) {
+  auto nsub_of = [&](int s) { return (slice_lanes(sh.n, s) + NW - 1) / NW; };
+  auto first_step = [&](int it) {
+    VStep st;
+    st.it = it;
+    st.s = (it / NRB) * spi;
+    st.s_end = min(sh.S, st.s + spi);
+    st.k = 0;
+    st.nsub = nsub_of(st.s);
+    return st;
+  };
+  auto next_step = [&](VStep st) {
+    if (++st.k < st.nsub) return st;
+    st.k = 0;
+    if (++st.s < st.s_end) {
+      st.nsub = nsub_of(st.s);
+      return st;
+    }
+    return first_step(st.it + 1);
+  };
+  // x tile of a step: x[beta][col0 .. col0 + 32 NW) for beta < b_pad (zero for
+  // beta >= b and lanes past the slice end), one 16-byte cp.async per thread
+  // for the first 128 threads (2 KB), x is L2-resident
+  auto load_x = [&](uint32_t dst, const VStep& st) {
     if (tid < 128) {
-      const int s = (int)(itx / NRB);
-      const int Ls = slice_lanes(sh.n, s);
-      const int bt = tid / (4 * P), c = tid % (4 * P);  // row of the tile, 16-byte chunk in the row
-      const bool ok = bt < b && k * P + c / 4 < Ls;
-      const __half* src = ok ? p.x + (size_t)bt * sh.n + s * kSliceCols + 32 * k * P + 8 * c : p.x;
-      cp_async_16(dst + 16u * tid, src, ok ? 16u : 0u);
+      const int Ls = slice_lanes(sh.n, st.s);
+      const int per_row = 4 * NW;  // 16-byte cells per tile row
+      const int bt = tid / per_row, c = tid % per_row;
+      const bool ok = bt < b && st.k * NW + c / 4 < Ls;
+      const __half* src = ok ? p.x + (size_t)bt * sh.n + st.s * kSliceCols + 32 * st.k * NW + 8 * c : p.x;
+      cp_async_16(dst + 16u * (uint32_t)xcell<V>(c, bt, NV), src, ok ? 16u : 0u);
     }
   };
-  // the (item, sub-slice) after (itx, k)
-  auto advance = [&](long long& itx, int& k) {
-    const int Ls = slice_lanes(sh.n, (int)(itx / NRB));
-    if (++k >= (Ls + P - 1) / P) {
-      k = 0;
-      ++itx;
-    }
+  // the lane's pointers at quad rq of a step (and whether its layout lane exists)
+  auto lane_ptr = [&](const VStep& st, int rq, bool& ok) {
+    const int Ls = slice_lanes(sh.n, st.s);
+    const int lay = st.k * NW + w;
+    ok = lay < Ls;
+    const int pl = ok ? lay : 0;
+    VPtr pt;
+    pt.KB = keys_bytes(sh, Ls);
+    pt.AB = alpha_bytes(sh, Ls);
+    pt.ZB = z_bytes(sh, Ls);
+    pt.kstride = (uint32_t)Ls * 16u;
+    const int r0 = rg * RPL;  // the lane's first row inside the quad
+    pt.kq = p.data + keys_base(sh, st.s, Ls) + (size_t)rq * pt.KB + pl * 16 + 4 * r0;
+    pt.aq = p.data + alpha_base(sh, st.s, Ls) + (size_t)rq * pt.AB + (uint32_t)(pl >> gsh) * sh.q * 8u + 2 * r0;
+    pt.zq = p.data + z_base(sh, st.s, Ls) + (size_t)rq * pt.ZB + (uint32_t)(pl >> gsh) * 8u + 2 * r0;
+    return pt;
   };
-  Ring<QT> ring[NB];
-  // first PD quads of sub-slice (itx, k) for this warp into ring[0..PD)
-  auto prologue = [&](long long itx, int k) {
-    const int s = (int)(itx / NRB), rb = (int)(itx % NRB);
-    const int Ls = slice_lanes(sh.n, s);
-    const int lay = k * P + pp;
-    const bool ok = lay < Ls;
-    const LaneAddr la = lane_addr(sh, p.data, s, Ls, ok ? lay : 0);
-    const int rq_w = rb * rbq + warp * QPW;
+  VRing<QT, RPL> ring[NB];
+  VPtr nxt;  // pointers of the next step, positioned after its prologue quads
+  bool nxt_ok;
+  auto prologue = [&](const VStep& st) {
+    const int rq_w = (st.it % NRB) * rbq + warp * QPW;
+    nxt = lane_ptr(st, rq_w, nxt_ok);
 #pragma unroll
-    for (int d = 0; d < PD; ++d) ring_load<QT, HAS_Z>(ring[d], ok && rq_w + d < sh.RQ, la, rq_w + d, q);
+    for (int d = 0; d < PD; ++d) vring_load<QT, RPL, HAS_Z>(ring[d], nxt_ok && rq_w + d < sh.RQ, nxt, q);
+  };
+  // bulk L2 prefetch of the item's row block in slice s (keys, scales, z)
+  auto prefetch_block = [&](int it, int s) {
+    const int a = (it % NRB) * rbq, e = min(sh.RQ, a + rbq);
+    prefetch_quads(sh, p.data, s, slice_lanes(sh.n, s), a, e);
   };
 
-  prologue(it0, 0);  // weights only: legal before the PDL wait
-  pdl_wait();        // x and the workspace belong to the preceding kernel until it completes
-  load_x(xt0, it0, 0);
+  VStep st = first_step(it0);
+  if (tid == 0) prefetch_block(st.it, st.s);
+  prologue(st);  // weights only: legal before the PDL wait
+  pdl_wait();    // x and the workspace belong to the preceding kernel until it completes
+  load_x(xt0, st);
   cp_async_wait_all();
   __syncthreads();
-  int e = 0;  // sub-slices processed: x tile e & 1
+  int e = 0;  // steps processed: x tile e & 1
 
-  for (long long it = it0; it < it1; ++it) {
-    const int s = (int)(it / NRB);
-    const int rb = (int)(it % NRB);
-    const int Ls = slice_lanes(sh.n, s);
-    const int nsub = (Ls + P - 1) / P;
-    const int rq_w = rb * rbq + warp * QPW;  // this warp's first quad
-    f32x2 acc01[QPW], acc23[QPW];
-
-    for (int k = 0; k < nsub; ++k, ++e) {
-      unsigned long long* tr = (p.trace && tid == 0 && it == it0 && k >= 2 && k < 4)
-                                   ? p.trace + (size_t)blockIdx.x * kTraceSlots + 4 * (k - 2) : nullptr;
-      if (tr) tr[0] = globaltimer_ns();
-      const int lay = k * P + pp;
-      const bool lane_ok = lay < Ls;
-      const LaneAddr la = lane_addr(sh, p.data, s, Ls, lane_ok ? lay : 0);
-      if (tr) tr[1] = globaltimer_ns();
-      {
-        const int l = lane, j = warp & 3, h = warp >> 2;
-        const int bt = l & (B - 1), pl = l >> bl;
-        build_table_part(sm.lut + table_offset(l, j), ((e & 1) ? xtile1 : xtile0) + (size_t)bt * 32 * P + (4 * pl + j) * 8,
-                         h);
-      }
+  while (st.it < it1) {
+    const int it = st.it;
+    const int rq_w = (it % NRB) * rbq + warp * QPW;  // this warp's first quad
+    const int nq = min(QPW, sh.RQ - rq_w);            // valid quads of this warp (may be <= 0)
+    f32x2 acc[QPW][RPL][NP];
+#pragma unroll
+    for (int t = 0; t < QPW; ++t)
+#pragma unroll
+      for (int rho = 0; rho < RPL; ++rho)
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp) acc[t][rho][pp] = 0ull;
+    const int sr = it / NRB;
+    while (st.it == it) {  // the slices and sub-slices of this item
+      VPtr cur = nxt;
+      const bool lane_ok = nxt_ok;
+      build_vtables<V>(sm.lut, (e & 1) ? xtile1 : xtile0, NV, tid);
       __syncthreads();
-      if (tr) tr[2] = globaltimer_ns();
-      long long itn = it;
-      int kn = k;
-      advance(itn, kn);
-      if (itn < it1) load_x((e & 1) ? xt0 : xt1, itn, kn);  // lands during the lookups
-      const float xsum = (HAS_Z && lane_ok) ? lane_xsum(sm.lut, lane) : 0.f;
+      const VStep sn = next_step(st);
+      if (sn.it < it1) {
+        load_x((e & 1) ? xt0 : xt1, sn);  // lands during the lookups
+        if (tid == 0 && (sn.s != st.s || sn.it != st.it)) prefetch_block(sn.it, sn.s);
+      }
+      f32x2 xs[NP];
+      if (HAS_Z) vword<V>(0xFFFFFFFFu, lc, xs);  // sum of x over the lane's 32 columns = sum_J T_J[255]
 #pragma unroll
       for (int t = 0; t < QPW; ++t) {
-        if (t + PD < QPW)
-          ring_load<QT, HAS_Z>(ring[(t + PD) % NB], lane_ok && rq_w + t + PD < sh.RQ, la, rq_w + t + PD, q);
-        ring_compute<QT, HAS_Z>(ring[t % NB], lc, xsum, acc01[t], acc23[t], q, k > 0);
+        if (t + PD < QPW) vring_load<QT, RPL, HAS_Z>(ring[(t + PD) % NB], lane_ok && t + PD < nq, cur, q);
+        vring_compute<V, QT, HAS_Z>(ring[t % NB], lc, xs, acc[t], q);
       }
-      if (itn < it1) prologue(itn, kn);  // next sub-slice's first quads fly during the barrier and rebuild
-      if (tr) tr[3] = globaltimer_ns();
+      if (sn.it < it1) prologue(sn);  // next step's first quads fly during the barrier and rebuild
       cp_async_wait_all();
       __syncthreads();  // every warp is done with the LUT; the next x tile is visible
+      st = sn;
+      ++e;
     }
-    // reduce over the P layout lanes that share a batch row (lane bits >= bl)
+    // reduce over the NW layout lanes of a row group (lane bits log2(NV) .. log2(LR)-1)
+    float* part = p.partial + (size_t)sr * sh.m4 * bpad;
 #pragma unroll
     for (int t = 0; t < QPW; ++t) {
-      float2 v01 = unpack2(acc01[t]), v23 = unpack2(acc23[t]);
-      for (int off = 16; off >= B; off >>= 1) {
-        v01.x += __shfl_xor_sync(kFull, v01.x, off);
-        v01.y += __shfl_xor_sync(kFull, v01.y, off);
-        v23.x += __shfl_xor_sync(kFull, v23.x, off);
-        v23.y += __shfl_xor_sync(kFull, v23.y, off);
-      }
-      const int rq = rq_w + t;
-      if (pp == 0 && beta < b && rq < sh.RQ) {
-        float* dst = p.partial + ((size_t)s * b + beta) * sh.m4 + 4 * rq;
-        *reinterpret_cast<float4*>(dst) = make_float4(v01.x, v01.y, v23.x, v23.y);
+#pragma unroll
+      for (int rho = 0; rho < RPL; ++rho) {
+        float2 f[NP];
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp) {
+          f[pp] = unpack2(acc[t][rho][pp]);
+          for (int off = NV; off < LR; off <<= 1) {
+            f[pp].x += __shfl_xor_sync(kFull, f[pp].x, off);
+            f[pp].y += __shfl_xor_sync(kFull, f[pp].y, off);
+          }
+        }
+        if (w == 0 && t < nq) {
+          float* dst = part + (size_t)(4 * (rq_w + t) + rg * RPL + rho) * bpad + v * V;
+          if constexpr (V == 4) *reinterpret_cast<float4*>(dst) = make_float4(f[0].x, f[0].y, f[1].x, f[1].y);
+          else *reinterpret_cast<float2*>(dst) = f[0];
+        }
       }
     }
   }
   pdl_launch_dependents();
+}
+
+// Batched cross-slice reduction: Y[beta][r] = sum_{s<S2} partial[s][r][beta]
+// in slice order (deterministic, R11), fp16 RNE (or fp32).  A block owns 64
+// rows: coalesced reads of the [row][b_pad] partials, transposed in shared
+// memory, coalesced writes of Y rows.
+__global__ void __launch_bounds__(256) lut_reduce_batched_kernel(const float* __restrict__ partial, int S2, int b,
+                                                                 int bpad, int m, int m4, __half* __restrict__ y,
+                                                                 float* __restrict__ yf) {
+  __shared__ float tile[32][65];
+  pdl_launch_dependents();
+  pdl_wait();
+  const int row0 = blockIdx.x * 64;
+  for (int e = threadIdx.x; e < 64 * bpad; e += 256) {
+    const int r = e / bpad, beta = e % bpad;
+    if (row0 + r >= m4) continue;
+    const float* src = partial + (size_t)(row0 + r) * bpad + beta;
+    float v = 0.f;
+    for (int s = 0; s < S2; ++s) v += __ldcg(src + (size_t)s * m4 * bpad);
+    tile[beta][r] = v;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < b * 64; e += 256) {
+    const int beta = e / 64, r = e % 64;
+    if (row0 + r >= m) continue;
+    const size_t o = (size_t)beta * m + row0 + r;
+    if (yf) yf[o] = tile[beta][r];
+    else y[o] = __float2half_rn(tile[beta][r]);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -642,12 +902,12 @@ static cudaLaunchAttribute g_pdl_attr = [] {
 }();
 
 template <typename K>
-static cudaError_t launch(K kernel, int grid, const KParams& p, cudaStream_t st) {
+static cudaError_t launch(K kernel, int grid, const KParams& p, cudaStream_t st, int threads = kThreads) {
   cudaError_t err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
   if (err != cudaSuccess) return err;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = st;
   cfg.attrs = &g_pdl_attr;
@@ -694,16 +954,56 @@ static cudaError_t launch_gemv_t(const KParams& p, int grid, cudaStream_t st) {
   return launch(lut_gemv_kernel<QT, HAS_Z, PD>, grid, p, st);
 }
 
-static int batched_qpw(const KParams& p) { return p.xmode == 6 ? 6 : (p.xmode == 7 ? 8 : kQPW); }
+// batched: V-wide slots (V = 2 only for b = 2), QPW row quads per warp per work item
+template <int V, int QT, bool HAS_Z>
+static cudaError_t launch_batched_v(const KParams& p, int grid, cudaStream_t st) {
+  if constexpr (QT <= 4) {
+    if (p.qpw == 8) return launch(lut_gemm_batched_kernel<V, QT, HAS_Z, 3, 8>, grid, p, st, kBThreads);
+    return launch(lut_gemm_batched_kernel<V, QT, HAS_Z, 3, 16>, grid, p, st, kBThreads);
+  } else {
+    return launch(lut_gemm_batched_kernel<V, QT, HAS_Z, 1, 8>, grid, p, st, kBThreads);
+  }
+}
 
 template <int QT, bool HAS_Z>
 static cudaError_t launch_batched_t(const KParams& p, int grid, cudaStream_t st) {
-  constexpr int PD = QT <= 4 ? 2 : 0;  // QPW % (PD + 1) == 0
-  if constexpr (QT <= 4) {
-    if (p.xmode == 6) return launch(lut_gemm_batched_kernel<QT, HAS_Z, PD, 6>, grid, p, st);
-    if (p.xmode == 7) return launch(lut_gemm_batched_kernel<QT, HAS_Z, 1, 8>, grid, p, st);
+  return p.b == 2 ? launch_batched_v<2, QT, HAS_Z>(p, grid, st) : launch_batched_v<4, QT, HAS_Z>(p, grid, st);
+}
+
+static cudaError_t launch_reduce_batched(const KParams& p, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((p.sh.m4 + 63) / 64);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cfg.attrs = &g_pdl_attr;
+  cfg.numAttrs = 1;
+  const int S2 = (p.sh.S + p.spi - 1) / p.spi;
+  return cudaLaunchKernelEx(&cfg, lut_reduce_batched_kernel, (const float*)p.partial, S2, p.b, 1 << p.bl, p.sh.m,
+                            p.sh.m4, p.y, p.yf);
+}
+
+// Work split of the batched kernel: items = (range of spi slices, row block of
+// 8 * qpw quads); pick (qpw, spi) minimising waves * spi * (per-sub-slice
+// lookup time + LUT rebuild time), ties to fewer partials (larger spi).
+static void plan_batched(const Shape& sh, int sms, KParams& p) {
+  double best = 1e30;
+  const int qpws[2] = {16, 8};
+  for (int qi = 0; qi < 2; ++qi) {
+    const int qpw = qpws[qi];
+    if (sh.q > 4 && qpw != 8) continue;
+    const long long nrb = (sh.RQ + kBWarps * qpw - 1) / (kBWarps * qpw);
+    for (int spi = 1; spi <= sh.S; ++spi) {
+      const long long items = (long long)((sh.S + spi - 1) / spi) * nrb;
+      const long long waves = (items + sms - 1) / sms;
+      const double cost = (double)waves * spi * (qpw * 128.0 * sh.q + 1200.0);
+      if (cost < best * 0.999 || (cost <= best * 1.001 && spi > p.spi)) {
+        best = std::min(best, cost);
+        p.qpw = qpw;
+        p.spi = spi;
+        p.items = items;
+      }
+    }
   }
-  return launch(lut_gemm_batched_kernel<QT, HAS_Z, PD, kQPW>, grid, p, st);
 }
 
 template <bool HAS_Z>
@@ -719,8 +1019,14 @@ static cudaError_t dispatch_q(const KParams& p, int grid, cudaStream_t st, bool 
 
 static size_t counters_bytes(const Shape&) { return 2u * kFusedMaxJ * 4u; }
 
+int batch_pad(int b) {
+  int bp = 1;
+  while (bp < b) bp <<= 1;
+  return b == 1 ? 1 : (b == 2 ? 2 : std::max(bp, 4));
+}
+
 size_t workspace_bytes(const Shape& sh, int b) {
-  return counters_bytes(sh) + ((size_t)sh.S * (size_t)b * (size_t)sh.m4 * 4u + 255) / 256 * 256;
+  return counters_bytes(sh) + ((size_t)sh.S * (size_t)batch_pad(b) * (size_t)sh.m4 * 4u + 255) / 256 * 256;
 }
 
 static int g_pf_steps = -1;
@@ -758,8 +1064,16 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
   p.sh = sh;
   p.b = b;
   int bl = 0;
-  while ((1 << bl) < b) ++bl;
+  while ((1 << bl) < batch_pad(b)) ++bl;
   p.bl = bl;
+  p.nv = b == 2 ? 1 : (1 << bl) / 4;
+  p.spi = 1;
+  p.qpw = 16;
+  {
+    int gs = 0;  // layout lane -> group shift (lanes are 32 columns); g > 1024: one group per slice
+    while (gs < 5 && (32 << gs) < sh.g) ++gs;
+    p.gsh = sh.g <= kSliceCols ? gs : 31;
+  }
   p.pf_steps = g_pf_steps;
   {
     static int pf_init = -1;
@@ -781,8 +1095,8 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
   if (!batched) {
     p.items = (long long)sh.S * sh.RQ;
   } else {
-    const int rbq = kWarps * batched_qpw(p);
-    p.items = (long long)sh.S * ((sh.RQ + rbq - 1) / rbq);
+    p.spi = 0;
+    plan_batched(sh, num_sms(), p);
   }
   int grid = (int)std::min<long long>((long long)num_sms(), p.items);
   // fused mode (b = 1): whole slices per CTA group, S*J CTAs with J per slice,
@@ -800,7 +1114,7 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
   if (e != cudaSuccess) return e;
   if (p.fused_J > 0) return cudaSuccess;  // reduced in-kernel
   if (p.xmode == 2) return cudaSuccess;  // experiment: no reduction (wrong results, timing only)
-  return launch_reduce(p, st);
+  return batched ? launch_reduce_batched(p, st) : launch_reduce(p, st);
 }
 
 }  // namespace lg

@@ -134,7 +134,7 @@ def test_gemv_shapes_full_parity(m, n, q, g, off):
 
 @pytest.mark.parametrize("b", [2, 3, 4, 5, 8, 16, 31, 32])
 @pytest.mark.parametrize("m,n,q,g,off", [(333, 1536, 3, 128, True), (1030, 4096, 2, 32, False),
-                                         (64, 2048, 6, 2048, True)])
+                                         (64, 2048, 6, 2048, True), (2500, 5152, 1, 32, True)])
 def test_batched_full_parity(b, m, n, q, g, off):
     d = gen_bcq(b * 13 + m, m, n, q, g, offset=off)
     X = gen_x(b + m, b, n)
