@@ -22,7 +22,7 @@ struct KParams {
   int bl;            // batched: log2 of the padded batch b_pad >= b (partials are [S2][m4][b_pad])
   int nv;            // batched: V-wide batch vectors per table entry slot group (b_pad = V * nv)
   int spi;           // batched: LUT slices per work item (split-K factor S2 = ceil(S / spi))
-  int qpw;           // batched: row quads per warp per work item
+  int qpw;           // batched: row quads per work item (256 or 128)
   int gsh;           // batched: layout lane -> slice-local group shift (31: one group per slice)
   int pf_steps;      // GEMV: L2 prefetch distance in 16-quad steps
   int pf_init;       // GEMV: 16-quad steps bulk-prefetched into L2 before the PDL wait

@@ -47,8 +47,6 @@ namespace lg {
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-constexpr int kBThreads = 256;         // batched kernel: 8 warps (255 registers per thread)
-constexpr int kBWarps = kBThreads / 32;
 constexpr int kMiscBytes = 8192;       // x double buffer (2 x 2 KB) + mbarriers + flags
 constexpr int kSmemBytes = 3 * 65536;  // LUT (128 KB) on a 64 KB boundary + misc, for any base
 constexpr int kPfSteps = 8;            // GEMV: L2 prefetch distance in 16-quad steps
@@ -504,11 +502,11 @@ __device__ __forceinline__ int xcell(int c, int bt, int NV) {
 // wv = s % LR.  T[k] = H(k >> 4) + (+-x0 +- x1) + (+-x2 +- x3): with
 // A1 = x0 - x1, A3 = x0 + x1 the low pair takes -A3, A1, -A1, A3 (likewise B
 // over x2, x3), so each entry costs one packed add after 4 adds per (h, pair).
-template <int V>
+template <int V, int NTH>
 __device__ __forceinline__ void build_vtables(uint32_t lut, const __half* tile, int NV, int tid) {
   constexpr int LR = 32 / V, NP = V / 2;
   constexpr int SPR = 2 * LR;                      // slots per region and key
-  constexpr int TPR = kBThreads / 2;               // threads per region
+  constexpr int TPR = NTH / 2;                     // threads per region
   constexpr int HPT = 16 * SPR / TPR;              // high nibbles per thread
   const int R = tid / TPR, rem = tid % TPR;
   const int s = rem % SPR, h0 = rem / SPR;
@@ -563,78 +561,81 @@ __device__ __forceinline__ void build_vtables(uint32_t lut, const __half* tile, 
   }
 }
 
-// One row quad's operands for one lane: the key words of its 4/V rows for q
-// planes, their scales (one fp16 per row, packed) per plane, and z.
-template <int QT, int RPL>
+// One row quad's operands for one lane: the key words of its 4 rows for q
+// planes (one 16-byte load each), their scales (4 fp16 per plane) and z.
+template <int QT>
 struct VRing {
-  uint32_t k[QT][RPL];
-  uint32_t a[QT];
-  uint32_t z;
+  uint4 k[QT];
+  uint2 a[QT];
+  uint2 z;
 };
 
 // The lane's running pointers into the three regions of one slice: plane i's
-// key word(s) of the next quad at kq + i * kstride, its scales at aq + 8 i,
-// its z at zq; each advances by the region's per-quad stride.
+// key words of the lane's next quad at kq + i * kstride, its scales at
+// aq + 8 i, its z at zq; each advances by V quads per step.
 struct VPtr {
   const uint8_t *kq, *aq, *zq;
-  uint32_t KB, AB, ZB, kstride;
+  uint32_t KB, AB, ZB, kstride;  // per-step strides (V quads) and the plane stride
 };
 
-template <int QT, int RPL, bool HAS_Z>
-__device__ __forceinline__ void vring_load(VRing<QT, RPL>& r, bool ok, VPtr& pt, int q) {
+template <int QT, bool HAS_Z>
+__device__ __forceinline__ void vring_load(VRing<QT>& r, bool ok, VPtr& pt, int q) {
 #pragma unroll
   for (int i = 0; i < QT; ++i) {
     if (QT <= 4 || i < q) {
       if (ok) {
-        const uint8_t* kp = pt.kq + i * pt.kstride;
-        if constexpr (RPL == 1) {
-          r.k[i][0] = ldg_nc_u32(kp);
-          r.a[i] = ldg_nc_u16(pt.aq + 8 * i);
-        } else {
-          const uint2 kk = ldg_nc_u2(kp);
-          r.k[i][0] = kk.x;
-          r.k[i][1] = kk.y;
-          r.a[i] = ldg_nc_u32(pt.aq + 8 * i);
-        }
+        r.k[i] = ldg_stream_u4(pt.kq + i * pt.kstride);
+        r.a[i] = ldg_nc_u2(pt.aq + 8 * i);
       } else {
-#pragma unroll
-        for (int u = 0; u < RPL; ++u) r.k[i][u] = 0u;
-        r.a[i] = 0u;
+        r.k[i] = make_uint4(0, 0, 0, 0);
+        r.a[i] = make_uint2(0, 0);
       }
     }
   }
-  if (HAS_Z) r.z = ok ? (RPL == 1 ? ldg_nc_u16(pt.zq) : ldg_nc_u32(pt.zq)) : 0u;
+  if (HAS_Z) r.z = ok ? ldg_nc_u2(pt.zq) : make_uint2(0, 0);
   pt.kq += pt.KB;
   pt.aq += pt.AB;
   if (HAS_Z) pt.zq += pt.ZB;
 }
 
-// acc[rho][p] (+)= sum_i alpha_i[rho] * (word lookups of row rho, plane i) + z[rho] * xsum
+// acc[rho][p] (+)= sum_i alpha_i[rho] * (word lookups of row rho, plane i) + z[rho] * xsum, rho < 4
 template <int V, int QT, bool HAS_Z>
-__device__ __forceinline__ void vring_compute(const VRing<QT, 4 / V>& r, uint32_t lc, const f32x2 (&xs)[V / 2],
-                                              f32x2 (&acc)[4 / V][V / 2], int q) {
-  constexpr int RPL = 4 / V, NP = V / 2;
+__device__ __forceinline__ void vring_compute(const VRing<QT>& r, uint32_t lc, const f32x2 (&xs)[V / 2],
+                                              f32x2 (&acc)[4][V / 2], int q) {
+  constexpr int NP = V / 2;
 #pragma unroll
   for (int i = 0; i < QT; ++i) {
     if (QT <= 4 || i < q) {
-      const float2 af = h2_to_f2(r.a[i]);  // RPL == 1: only .x is meaningful
+      const uint32_t kw[4] = {r.k[i].x, r.k[i].y, r.k[i].z, r.k[i].w};
+      const float2 a01 = h2_to_f2(r.a[i].x), a23 = h2_to_f2(r.a[i].y);
+      const float al[4] = {a01.x, a01.y, a23.x, a23.y};
+      // all 16 lookups of the plane are issued before the first add (ILP over
+      // the LDS latency), then summed per row and scaled
+      f32x2 t[4][4][NP];
 #pragma unroll
-      for (int rho = 0; rho < RPL; ++rho) {
-        f32x2 s[NP];
-        vword<V>(r.k[i][rho], lc, s);
-        const float al = rho == 0 ? af.x : af.y;
-        const f32x2 aa = pack2(al, al);
+      for (int rho = 0; rho < 4; ++rho) {
+        vlut<V, 0>(kw[rho], lc, t[rho][0]);
+        vlut<V, 1>(kw[rho], lc, t[rho][1]);
+        vlut<V, 2>(kw[rho], lc, t[rho][2]);
+        vlut<V, 3>(kw[rho], lc, t[rho][3]);
+      }
 #pragma unroll
-        for (int p = 0; p < NP; ++p) acc[rho][p] = fma2(aa, s[p], acc[rho][p]);
+      for (int rho = 0; rho < 4; ++rho) {
+        const f32x2 aa = pack2(al[rho], al[rho]);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          const f32x2 s = add2(add2(t[rho][0][p], t[rho][1][p]), add2(t[rho][2][p], t[rho][3][p]));
+          acc[rho][p] = fma2(aa, s, acc[rho][p]);
+        }
       }
     }
   }
   if (HAS_Z) {
-    const float2 zf = h2_to_f2(r.z);
+    const float2 z01 = h2_to_f2(r.z.x), z23 = h2_to_f2(r.z.y);
+    const float zv[4] = {z01.x, z01.y, z23.x, z23.y};
 #pragma unroll
-    for (int rho = 0; rho < RPL; ++rho) {
-      const float zv = rho == 0 ? zf.x : zf.y;
-      const f32x2 zz = pack2(zv, zv);
+    for (int rho = 0; rho < 4; ++rho) {
+      const f32x2 zz = pack2(zv[rho], zv[rho]);
 #pragma unroll
       for (int p = 0; p < NP; ++p) acc[rho][p] = fma2(zz, xs[p], acc[rho][p]);
     }
@@ -648,18 +649,21 @@ struct VStep {
   int nsub;   // sub-slices of slice s
 };
 
-template <int V, int QT, bool HAS_Z, int PD, int QPW>
-__global__ void __launch_bounds__(kBThreads, 1) lut_gemm_batched_kernel(const KParams p) {
+// Lanes: lane = qi * LR + wv: quad qi of each group of V consecutive quads
+// (all 4 rows of it), wv = w * NV + v as above.  A warp owns QPW consecutive
+// quads of the work item's row block, processed as QPW / V steps.
+template <int V, int QT, bool HAS_Z, int PD, int QPW, int NTH>
+__global__ void __launch_bounds__(NTH, 1) lut_gemm_batched_kernel(const KParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  constexpr int LR = 32 / V, RPL = 4 / V, NP = V / 2, NB = PD + 1;
-  static_assert(QPW % NB == 0, "the ring restarts at buffer 0 every sub-slice");
+  constexpr int LR = 32 / V, NP = V / 2, NB = PD + 1, NT = QPW / V;
+  static_assert(QPW % V == 0 && NT % NB == 0, "the ring restarts at buffer 0 every sub-slice");
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(kFull, tid >> 5, 0);
   const Shape sh = p.sh;
   const int q = QT <= 4 ? QT : sh.q;
   const int NV = p.nv, NW = LR / NV, bpad = V * NV, b = p.b, spi = p.spi;
-  const int rg = lane / LR, wv = lane % LR, w = wv / NV, v = wv % NV;
-  const int rbq = kBWarps * QPW;  // row quads per work item
+  const int qi = lane / LR, wv = lane % LR, w = wv / NV, v = wv % NV;
+  const int rbq = (NTH / 32) * QPW;  // row quads per work item
   const int NRB = (sh.RQ + rbq - 1) / rbq;
   const int it0 = (int)(p.items * blockIdx.x / gridDim.x);
   const int it1 = (int)(p.items * (blockIdx.x + 1) / gridDim.x);
@@ -704,40 +708,35 @@ __global__ void __launch_bounds__(kBThreads, 1) lut_gemm_batched_kernel(const KP
       cp_async_16(dst + 16u * (uint32_t)xcell<V>(c, bt, NV), src, ok ? 16u : 0u);
     }
   };
-  // the lane's pointers at quad rq of a step (and whether its layout lane exists)
-  auto lane_ptr = [&](const VStep& st, int rq, bool& ok) {
+  // the lane's pointers at its quad of the warp's first group (quad rq_w + qi)
+  auto lane_ptr = [&](const VStep& st, int rq_w, bool& ok) {
     const int Ls = slice_lanes(sh.n, st.s);
     const int lay = st.k * NW + w;
     ok = lay < Ls;
     const int pl = ok ? lay : 0;
+    const int rq = rq_w + qi;
     VPtr pt;
-    pt.KB = keys_bytes(sh, Ls);
-    pt.AB = alpha_bytes(sh, Ls);
-    pt.ZB = z_bytes(sh, Ls);
+    const uint32_t KB = keys_bytes(sh, Ls), AB = alpha_bytes(sh, Ls), ZB = z_bytes(sh, Ls);
+    pt.KB = KB * V;
+    pt.AB = AB * V;
+    pt.ZB = ZB * V;
     pt.kstride = (uint32_t)Ls * 16u;
-    const int r0 = rg * RPL;  // the lane's first row inside the quad
-    pt.kq = p.data + keys_base(sh, st.s, Ls) + (size_t)rq * pt.KB + pl * 16 + 4 * r0;
-    pt.aq = p.data + alpha_base(sh, st.s, Ls) + (size_t)rq * pt.AB + (uint32_t)(pl >> gsh) * sh.q * 8u + 2 * r0;
-    pt.zq = p.data + z_base(sh, st.s, Ls) + (size_t)rq * pt.ZB + (uint32_t)(pl >> gsh) * 8u + 2 * r0;
+    pt.kq = p.data + keys_base(sh, st.s, Ls) + (size_t)rq * KB + pl * 16;
+    pt.aq = p.data + alpha_base(sh, st.s, Ls) + (size_t)rq * AB + (uint32_t)(pl >> gsh) * sh.q * 8u;
+    pt.zq = p.data + z_base(sh, st.s, Ls) + (size_t)rq * ZB + (uint32_t)(pl >> gsh) * 8u;
     return pt;
   };
-  VRing<QT, RPL> ring[NB];
-  VPtr nxt;  // pointers of the next step, positioned after its prologue quads
+  VRing<QT> ring[NB];
+  VPtr nxt;  // pointers of the next step, positioned after its prologue groups
   bool nxt_ok;
   auto prologue = [&](const VStep& st) {
     const int rq_w = (st.it % NRB) * rbq + warp * QPW;
     nxt = lane_ptr(st, rq_w, nxt_ok);
 #pragma unroll
-    for (int d = 0; d < PD; ++d) vring_load<QT, RPL, HAS_Z>(ring[d], nxt_ok && rq_w + d < sh.RQ, nxt, q);
-  };
-  // bulk L2 prefetch of the item's row block in slice s (keys, scales, z)
-  auto prefetch_block = [&](int it, int s) {
-    const int a = (it % NRB) * rbq, e = min(sh.RQ, a + rbq);
-    prefetch_quads(sh, p.data, s, slice_lanes(sh.n, s), a, e);
+    for (int d = 0; d < PD; ++d) vring_load<QT, HAS_Z>(ring[d], nxt_ok && rq_w + V * d + qi < sh.RQ, nxt, q);
   };
 
   VStep st = first_step(it0);
-  if (tid == 0) prefetch_block(st.it, st.s);
   prologue(st);  // weights only: legal before the PDL wait
   pdl_wait();    // x and the workspace belong to the preceding kernel until it completes
   load_x(xt0, st);
@@ -748,30 +747,27 @@ __global__ void __launch_bounds__(kBThreads, 1) lut_gemm_batched_kernel(const KP
   while (st.it < it1) {
     const int it = st.it;
     const int rq_w = (it % NRB) * rbq + warp * QPW;  // this warp's first quad
-    const int nq = min(QPW, sh.RQ - rq_w);            // valid quads of this warp (may be <= 0)
-    f32x2 acc[QPW][RPL][NP];
+    const int nql = sh.RQ - (rq_w + qi);             // quads from the lane's first one to the end
+    f32x2 acc[NT][4][NP];
 #pragma unroll
-    for (int t = 0; t < QPW; ++t)
+    for (int t = 0; t < NT; ++t)
 #pragma unroll
-      for (int rho = 0; rho < RPL; ++rho)
+      for (int rho = 0; rho < 4; ++rho)
 #pragma unroll
         for (int pp = 0; pp < NP; ++pp) acc[t][rho][pp] = 0ull;
     const int sr = it / NRB;
     while (st.it == it) {  // the slices and sub-slices of this item
       VPtr cur = nxt;
       const bool lane_ok = nxt_ok;
-      build_vtables<V>(sm.lut, (e & 1) ? xtile1 : xtile0, NV, tid);
+      build_vtables<V, NTH>(sm.lut, (e & 1) ? xtile1 : xtile0, NV, tid);
       __syncthreads();
       const VStep sn = next_step(st);
-      if (sn.it < it1) {
-        load_x((e & 1) ? xt0 : xt1, sn);  // lands during the lookups
-        if (tid == 0 && (sn.s != st.s || sn.it != st.it)) prefetch_block(sn.it, sn.s);
-      }
+      if (sn.it < it1) load_x((e & 1) ? xt0 : xt1, sn);  // lands during the lookups
       f32x2 xs[NP];
       if (HAS_Z) vword<V>(0xFFFFFFFFu, lc, xs);  // sum of x over the lane's 32 columns = sum_J T_J[255]
 #pragma unroll
-      for (int t = 0; t < QPW; ++t) {
-        if (t + PD < QPW) vring_load<QT, RPL, HAS_Z>(ring[(t + PD) % NB], lane_ok && t + PD < nq, cur, q);
+      for (int t = 0; t < NT; ++t) {
+        if (t + PD < NT) vring_load<QT, HAS_Z>(ring[(t + PD) % NB], lane_ok && V * (t + PD) < nql, cur, q);
         vring_compute<V, QT, HAS_Z>(ring[t % NB], lc, xs, acc[t], q);
       }
       if (sn.it < it1) prologue(sn);  // next step's first quads fly during the barrier and rebuild
@@ -780,12 +776,12 @@ __global__ void __launch_bounds__(kBThreads, 1) lut_gemm_batched_kernel(const KP
       st = sn;
       ++e;
     }
-    // reduce over the NW layout lanes of a row group (lane bits log2(NV) .. log2(LR)-1)
+    // reduce over the NW layout lanes of a quad (lane bits log2(NV) .. log2(LR)-1)
     float* part = p.partial + (size_t)sr * sh.m4 * bpad;
 #pragma unroll
-    for (int t = 0; t < QPW; ++t) {
+    for (int t = 0; t < NT; ++t) {
 #pragma unroll
-      for (int rho = 0; rho < RPL; ++rho) {
+      for (int rho = 0; rho < 4; ++rho) {
         float2 f[NP];
 #pragma unroll
         for (int pp = 0; pp < NP; ++pp) {
@@ -795,8 +791,8 @@ __global__ void __launch_bounds__(kBThreads, 1) lut_gemm_batched_kernel(const KP
             f[pp].y += __shfl_xor_sync(kFull, f[pp].y, off);
           }
         }
-        if (w == 0 && t < nq) {
-          float* dst = part + (size_t)(4 * (rq_w + t) + rg * RPL + rho) * bpad + v * V;
+        if (w == 0 && V * t < nql) {
+          float* dst = part + (size_t)(4 * (rq_w + qi + V * t) + rho) * bpad + v * V;
           if constexpr (V == 4) *reinterpret_cast<float4*>(dst) = make_float4(f[0].x, f[0].y, f[1].x, f[1].y);
           else *reinterpret_cast<float2*>(dst) = f[0];
         }
@@ -954,14 +950,19 @@ static cudaError_t launch_gemv_t(const KParams& p, int grid, cudaStream_t st) {
   return launch(lut_gemv_kernel<QT, HAS_Z, PD>, grid, p, st);
 }
 
-// batched: V-wide slots (V = 2 only for b = 2), QPW row quads per warp per work item
+// batched: V-wide slots (V = 2 only for b = 2); p.qpw = row quads per work item
+// (256 or 128).  V = 2 runs 16 warps (128 registers: 4 rows x 2 batch x 16
+// quads of accumulators), V = 4 and q > 4 run 8 warps (255 registers).
 template <int V, int QT, bool HAS_Z>
 static cudaError_t launch_batched_v(const KParams& p, int grid, cudaStream_t st) {
-  if constexpr (QT <= 4) {
-    if (p.qpw == 8) return launch(lut_gemm_batched_kernel<V, QT, HAS_Z, 3, 8>, grid, p, st, kBThreads);
-    return launch(lut_gemm_batched_kernel<V, QT, HAS_Z, 3, 16>, grid, p, st, kBThreads);
+  if constexpr (QT <= 4 && V == 2) {
+    if (p.qpw == 128) return launch(lut_gemm_batched_kernel<V, QT, HAS_Z, 1, 8, 512>, grid, p, st, 512);
+    return launch(lut_gemm_batched_kernel<V, QT, HAS_Z, 1, 16, 512>, grid, p, st, 512);
+  } else if constexpr (QT <= 4) {
+    if (p.qpw == 128) return launch(lut_gemm_batched_kernel<V, QT, HAS_Z, 1, 16, 256>, grid, p, st, 256);
+    return launch(lut_gemm_batched_kernel<V, QT, HAS_Z, 1, 32, 256>, grid, p, st, 256);
   } else {
-    return launch(lut_gemm_batched_kernel<V, QT, HAS_Z, 1, 8>, grid, p, st, kBThreads);
+    return launch(lut_gemm_batched_kernel<V, QT, HAS_Z, 1, 16, 256>, grid, p, st, 256);
   }
 }
 
@@ -983,22 +984,27 @@ static cudaError_t launch_reduce_batched(const KParams& p, cudaStream_t st) {
 }
 
 // Work split of the batched kernel: items = (range of spi slices, row block of
-// 8 * qpw quads); pick (qpw, spi) minimising waves * spi * (per-sub-slice
-// lookup time + LUT rebuild time), ties to fewer partials (larger spi).
+// rbq = 256 or 128 quads); pick (rbq, spi) minimising waves * spi * (per-sub-
+// slice lookup time + LUT rebuild time), ties to fewer partials (larger spi).
 static void plan_batched(const Shape& sh, int sms, KParams& p) {
   double best = 1e30;
-  const int qpws[2] = {16, 8};
+  const int rbqs[2] = {256, 128};
+  static int force = -1;
+  if (force < 0) {
+    const char* env = getenv("LUTGEMM_BRBQ");  // tuning knob: force 256 or 128
+    force = env ? atoi(env) : 0;
+  }
   for (int qi = 0; qi < 2; ++qi) {
-    const int qpw = qpws[qi];
-    if (sh.q > 4 && qpw != 8) continue;
-    const long long nrb = (sh.RQ + kBWarps * qpw - 1) / (kBWarps * qpw);
+    const int rbq = rbqs[qi];
+    if ((sh.q > 4 && rbq != 128) || (force && rbq != force)) continue;
+    const long long nrb = (sh.RQ + rbq - 1) / rbq;
     for (int spi = 1; spi <= sh.S; ++spi) {
       const long long items = (long long)((sh.S + spi - 1) / spi) * nrb;
       const long long waves = (items + sms - 1) / sms;
-      const double cost = (double)waves * spi * (qpw * 128.0 * sh.q + 1200.0);
+      const double cost = (double)waves * spi * (rbq * 16.0 * sh.q + 1200.0);
       if (cost < best * 0.999 || (cost <= best * 1.001 && spi > p.spi)) {
         best = std::min(best, cost);
-        p.qpw = qpw;
+        p.qpw = rbq;
         p.spi = spi;
         p.items = items;
       }
@@ -1068,7 +1074,7 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
   p.bl = bl;
   p.nv = b == 2 ? 1 : (1 << bl) / 4;
   p.spi = 1;
-  p.qpw = 16;
+  p.qpw = 256;
   {
     int gs = 0;  // layout lane -> group shift (lanes are 32 columns); g > 1024: one group per slice
     while (gs < 5 && (32 << gs) < sh.g) ++gs;

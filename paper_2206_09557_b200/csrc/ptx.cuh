@@ -53,6 +53,10 @@ __device__ __forceinline__ void sts_b64x2(uint32_t addr, unsigned long long a, u
   asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(addr), "l"(a), "l"(b) : "memory");
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 __device__ __forceinline__ uint32_t ldg_nc_u32(const void* p) {
   uint32_t r;
   asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(r) : "l"(p));
