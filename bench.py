@@ -41,10 +41,12 @@ METRIC = "LUT-GEMM GEMV us and achieved HBM GB/s (% of B200 peak) at q=3,g=128"
 UNIT = "GB/s"
 
 
-def algorithmic_bytes(m: int, n: int, q: int, g: int, b: int = 1, offset: bool = False) -> int:
-    """B_alg = m n q/8 (planes) + 2 m (n/g) q (alpha) [+ 2 m (n/g) z] + 2 n b (x) + 2 m b (y)."""
+def algorithmic_bytes(m: int, n: int, q: int, g: int, b: int = 1, offset: bool = False, compact: bool = False) -> int:
+    """B_alg = m n q/8 (planes) + 2 m (n/g) q (alpha) [+ 2 m (n/g) z] + 2 n b (x) + 2 m b (y)  (SURVEY 8(d));
+    the compact uniform format stores one scale s per group instead of q alphas (NEXT-2, has z)."""
     G = n // g
-    return m * n * q // 8 + 2 * m * G * q + (2 * m * G if offset else 0) + 2 * n * b + 2 * m * b
+    qa = 1 if compact else q
+    return m * n * q // 8 + 2 * m * G * qa + (2 * m * G if (offset or compact) else 0) + 2 * n * b + 2 * m * b
 
 
 def measured_peaks() -> dict:

@@ -64,11 +64,22 @@ typedef enum {
 typedef struct {
   int32_t m, n, q, g;
   int32_t has_offset; /* 1: extended BCQ with bias z (Eq. 3); 0: z = 0 */
-  int32_t reserved;
+  int32_t format;     /* LUTGEMM_FMT_BCQ or LUTGEMM_FMT_UNIFORM_COMPACT (set by lutgemm_pack_bcq) */
   void* data;
 } lutgemm_weight;
 
-enum { LUTGEMM_SRC_BCQ = 0, LUTGEMM_SRC_UNIFORM = 1 };
+/* Stored-scale formats of a packed weight.
+ *  BCQ: q fp16 scales alpha_i per (row, group) (+ z if has_offset) -- any
+ *       extended-BCQ weight (Eq. 3, group-wise P:L296).
+ *  UNIFORM_COMPACT: a uniform-quantized weight (App. C) keeps ONE
+ *       fp16 scale s and the fp16 bias z per (row, group); the kernels derive
+ *       alpha_i = 2^(i-1) s exactly (power-of-two scaling).  Same product as the
+ *       BCQ conversion of the same source, with q-1 fewer scale loads per group
+ *       (Table 5 counts one scale per group, R18). has_offset = 1. */
+enum { LUTGEMM_FMT_BCQ = 0, LUTGEMM_FMT_UNIFORM_COMPACT = 1 };
+
+/* UNIFORM_COMPACT: as UNIFORM, but packed into the UNIFORM_COMPACT format. */
+enum { LUTGEMM_SRC_BCQ = 0, LUTGEMM_SRC_UNIFORM = 1, LUTGEMM_SRC_UNIFORM_COMPACT = 2 };
 
 /* Source of a pack call, canonical layout, all device pointers.
  * BCQ (non-uniform, Eq. 3):
@@ -109,15 +120,22 @@ const char* lutgemm_last_error(void);
  * m4 = 4*ceil(m/4).  Pure host computation. */
 lutgemm_status lutgemm_packed_bytes(int m, int n, int q, int g, int has_offset, size_t* bytes);
 
+/* As lutgemm_packed_bytes for a given format (LUTGEMM_FMT_*); the
+ * UNIFORM_COMPACT format implies has_offset = 1. */
+lutgemm_status lutgemm_packed_bytes_fmt(int m, int n, int q, int g, int has_offset, int format, size_t* bytes);
+
 /* Repack a canonical BCQ or uniform source into dst->data (which the caller
- * allocated with lutgemm_packed_bytes(..., has_offset) bytes, has_offset = 1
- * for UNIFORM, and for BCQ iff src->offset != NULL).  The call fills dst->m,
- * n, q, g, has_offset.  Offline step (App. C "two-step methodology",
- * P:L615-620); asynchronous on `stream`. */
+ * allocated with lutgemm_packed_bytes_fmt(..., has_offset, format) bytes:
+ * has_offset = 1 for UNIFORM / UNIFORM_COMPACT, and for BCQ iff src->offset !=
+ * NULL; format = UNIFORM_COMPACT for that source kind, else BCQ).  The call
+ * fills dst->m, n, q, g, has_offset, format.  Offline step (App. C "two-step
+ * methodology"); asynchronous on `stream`. */
 lutgemm_status lutgemm_pack_bcq(const lutgemm_pack_src* src, lutgemm_weight* dst, void* stream);
 
 /* Inverse of the BCQ pack (test-only): native -> canonical planes / alpha /
- * offset (offset may be NULL).  Bit-exact round trip. */
+ * offset (offset may be NULL).  Bit-exact round trip.  A UNIFORM_COMPACT
+ * weight unpacks to the alpha_i = 2^(i-1) s of its stored s (fp16-exact for
+ * the normal s the generators draw), i.e. to the UNIFORM pack of the same source. */
 lutgemm_status lutgemm_unpack_bcq(const lutgemm_weight* w, uint32_t* planes, uint16_t* alpha,
                                   uint16_t* offset, void* stream);
 

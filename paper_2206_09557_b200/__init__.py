@@ -5,6 +5,8 @@ of ``include/lutgemm.h``); ``lutgemm`` is its ctypes binding.  Importing this
 package without the built library raises -- there is no CPU fallback.
 """
 from .lutgemm import (  # noqa: F401
+    FMT_BCQ,
+    FMT_UNIFORM_COMPACT,
     LIB_PATH,
     LutgemmError,
     PackedBCQ,

@@ -11,7 +11,9 @@
 // blocks; misaligned 512-byte warp loads would over-fetch):
 //
 //   keys  [RQ][q][L_s][4 rows] uint32   -> q*L_s*16 bytes per row quad
-//   alpha [RQ][gps_s][q][4 rows] fp16   -> q*gps_s*8 bytes per row quad
+//   alpha [RQ][gps_s][qa][4 rows] fp16  -> qa*gps_s*8 bytes per row quad
+//         (qa = q; compact uniform format: qa = 1, the stored value is s and
+//         alpha_i = 2^(i-1) s is derived in the kernel, App. C)
 //   z     [RQ][gps_s][4 rows] fp16      -> gps_s*8 bytes per row quad (has_offset)
 //
 // gps_s = groups per slice = 32*L_s/g when g <= 1024 (g must divide 1024), else
@@ -32,12 +34,14 @@ constexpr int kLutBytes = 128 * 1024;
 
 struct Shape {
   int m, n, q, g, has_z;
+  int compact;  // 1: uniform-compact format (one stored scale s per group, has_z = 1)
   int m4, RQ, G, S;
 };
 
-__host__ __device__ inline Shape make_shape(int m, int n, int q, int g, int has_z) {
+__host__ __device__ inline Shape make_shape(int m, int n, int q, int g, int has_z, int compact = 0) {
   Shape s;
-  s.m = m; s.n = n; s.q = q; s.g = g; s.has_z = has_z ? 1 : 0;
+  s.m = m; s.n = n; s.q = q; s.g = g; s.has_z = (has_z || compact) ? 1 : 0;
+  s.compact = compact ? 1 : 0;
   s.m4 = (m + 3) / 4 * 4;
   s.RQ = s.m4 / 4;
   s.G = n / g;
@@ -66,8 +70,10 @@ __host__ __device__ inline int global_group(const Shape& sh, int s, int k) {
 
 // bytes per row quad in each region
 __host__ __device__ inline uint32_t keys_bytes(const Shape& sh, int Ls) { return (uint32_t)sh.q * Ls * 16u; }
+// stored scales per (row, group): q alphas, or the single s of the compact format
+__host__ __device__ inline int scale_planes(const Shape& sh) { return sh.compact ? 1 : sh.q; }
 __host__ __device__ inline uint32_t alpha_bytes(const Shape& sh, int Ls) {
-  return (uint32_t)sh.q * slice_groups(sh, Ls) * 8u;
+  return (uint32_t)scale_planes(sh) * slice_groups(sh, Ls) * 8u;
 }
 __host__ __device__ inline uint32_t z_bytes(const Shape& sh, int Ls) {
   return sh.has_z ? (uint32_t)slice_groups(sh, Ls) * 8u : 0u;
@@ -105,7 +111,7 @@ __host__ __device__ inline size_t key_at(const Shape& sh, int s, int Ls, int rq,
   return keys_base(sh, s, Ls) + (size_t)rq * keys_bytes(sh, Ls) + ((uint32_t)i * Ls + p) * 16u + 4u * r4;
 }
 __host__ __device__ inline size_t alpha_at(const Shape& sh, int s, int Ls, int rq, int i, int k, int r4) {
-  return alpha_base(sh, s, Ls) + (size_t)rq * alpha_bytes(sh, Ls) + ((uint32_t)k * sh.q + i) * 8u + 2u * r4;
+  return alpha_base(sh, s, Ls) + (size_t)rq * alpha_bytes(sh, Ls) + ((uint32_t)k * scale_planes(sh) + i) * 8u + 2u * r4;
 }
 __host__ __device__ inline size_t z_at(const Shape& sh, int s, int Ls, int rq, int k, int r4) {
   return z_base(sh, s, Ls) + (size_t)rq * z_bytes(sh, Ls) + (uint32_t)k * 8u + 2u * r4;

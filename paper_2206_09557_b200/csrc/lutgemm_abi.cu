@@ -68,7 +68,15 @@ lutgemm_status check_weight(const lutgemm_weight* w) {
   if (!w->data) return fail(LUTGEMM_ERR_INVALID_ARG, "weight data is NULL");
   if (w->has_offset != 0 && w->has_offset != 1) return fail(LUTGEMM_ERR_INVALID_ARG, "has_offset must be 0 or 1");
   if (!aligned(w->data, 16)) return fail(LUTGEMM_ERR_MISALIGNED, "weight data must be 16-byte aligned");
+  if (w->format != LUTGEMM_FMT_BCQ && w->format != LUTGEMM_FMT_UNIFORM_COMPACT)
+    return fail(LUTGEMM_ERR_INVALID_ARG, "bad weight format %d", w->format);
+  if (w->format == LUTGEMM_FMT_UNIFORM_COMPACT && !w->has_offset)
+    return fail(LUTGEMM_ERR_INVALID_ARG, "the uniform-compact format carries an offset (has_offset = 1)");
   return LUTGEMM_OK;
+}
+
+lg::Shape weight_shape(const lutgemm_weight* w) {
+  return lg::make_shape(w->m, w->n, w->q, w->g, w->has_offset, w->format == LUTGEMM_FMT_UNIFORM_COMPACT);
 }
 
 lutgemm_status product(const lutgemm_weight* w, const uint16_t* X, int b, uint16_t* Y, float* Yf, void* ws,
@@ -81,7 +89,7 @@ lutgemm_status product(const lutgemm_weight* w, const uint16_t* X, int b, uint16
   if (!aligned(ws, 16)) return fail(LUTGEMM_ERR_MISALIGNED, "ws must be 16-byte aligned");
   if (Y && !aligned(Y, 2)) return fail(LUTGEMM_ERR_MISALIGNED, "y must be 2-byte aligned");
   if (Yf && !aligned(Yf, 4)) return fail(LUTGEMM_ERR_MISALIGNED, "yf must be 4-byte aligned");
-  const lg::Shape sh = lg::make_shape(w->m, w->n, w->q, w->g, w->has_offset);
+  const lg::Shape sh = weight_shape(w);
   const size_t need = lg::workspace_bytes(sh, b);
   if (ws_bytes < need) return fail(LUTGEMM_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, need);
   st = check_device();
@@ -107,11 +115,22 @@ lutgemm_status lutgemm_packed_bytes(int m, int n, int q, int g, int has_offset, 
   return LUTGEMM_OK;
 }
 
+lutgemm_status lutgemm_packed_bytes_fmt(int m, int n, int q, int g, int has_offset, int format, size_t* bytes) {
+  lutgemm_status st = check_shape(m, n, q, g);
+  if (st != LUTGEMM_OK) return st;
+  if (!bytes) return fail(LUTGEMM_ERR_INVALID_ARG, "bytes is NULL");
+  if (format != LUTGEMM_FMT_BCQ && format != LUTGEMM_FMT_UNIFORM_COMPACT)
+    return fail(LUTGEMM_ERR_INVALID_ARG, "bad format %d", format);
+  *bytes = lg::packed_bytes(lg::make_shape(m, n, q, g, has_offset, format == LUTGEMM_FMT_UNIFORM_COMPACT));
+  return LUTGEMM_OK;
+}
+
 lutgemm_status lutgemm_pack_bcq(const lutgemm_pack_src* src, lutgemm_weight* dst, void* stream) {
   if (!src || !dst) return fail(LUTGEMM_ERR_INVALID_ARG, "src/dst is NULL");
   lutgemm_status st = check_shape(src->m, src->n, src->q, src->g);
   if (st != LUTGEMM_OK) return st;
-  const bool uniform = src->kind == LUTGEMM_SRC_UNIFORM;
+  const bool compact = src->kind == LUTGEMM_SRC_UNIFORM_COMPACT;
+  const bool uniform = src->kind == LUTGEMM_SRC_UNIFORM || compact;
   if (src->kind != LUTGEMM_SRC_BCQ && !uniform) return fail(LUTGEMM_ERR_INVALID_ARG, "bad src kind %d", src->kind);
   if (uniform) {
     if (!src->codes || !src->scale || !src->zero)
@@ -128,7 +147,7 @@ lutgemm_status lutgemm_pack_bcq(const lutgemm_pack_src* src, lutgemm_weight* dst
     return fail(LUTGEMM_ERR_MISALIGNED, "source buffers must be element-aligned");
   st = check_device();
   if (st != LUTGEMM_OK) return st;
-  const lg::Shape sh = lg::make_shape(src->m, src->n, src->q, src->g, has_offset);
+  const lg::Shape sh = lg::make_shape(src->m, src->n, src->q, src->g, has_offset, compact);
   cudaError_t e;
   if (uniform)
     e = lg::run_pack_uniform(sh, src->codes, src->scale, src->zero, dst->data, static_cast<cudaStream_t>(stream));
@@ -140,7 +159,7 @@ lutgemm_status lutgemm_pack_bcq(const lutgemm_pack_src* src, lutgemm_weight* dst
   dst->q = src->q;
   dst->g = src->g;
   dst->has_offset = has_offset;
-  dst->reserved = 0;
+  dst->format = compact ? LUTGEMM_FMT_UNIFORM_COMPACT : LUTGEMM_FMT_BCQ;
   return LUTGEMM_OK;
 }
 
@@ -151,7 +170,7 @@ lutgemm_status lutgemm_unpack_bcq(const lutgemm_weight* w, uint32_t* planes, uin
   if (offset && !w->has_offset) return fail(LUTGEMM_ERR_INVALID_ARG, "weight has no offset to unpack");
   st = check_device();
   if (st != LUTGEMM_OK) return st;
-  const lg::Shape sh = lg::make_shape(w->m, w->n, w->q, w->g, w->has_offset);
+  const lg::Shape sh = weight_shape(w);
   cudaError_t e = lg::run_unpack(sh, w->data, planes, alpha, offset, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "unpack kernel launch");
   return LUTGEMM_OK;

@@ -49,7 +49,6 @@ constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMiscBytes = 8192;       // x double buffer (2 x 2 KB) + mbarriers + flags
 constexpr int kSmemBytes = 3 * 65536;  // LUT (128 KB) on a 64 KB boundary + misc, for any base
-constexpr int kPfSteps = 8;            // GEMV: L2 prefetch distance in 16-quad steps
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kFusedMaxJ = 256;        // max CTAs per slice in the fused-reduction mode
 
@@ -201,8 +200,9 @@ __device__ __forceinline__ void prefetch_quads(const Shape& sh, const uint8_t* d
   if (zb) pf(data + z_base(sh, s, Ls), (size_t)a * zb, (size_t)b * zb);
 }
 
-template <int QT, bool HAS_Z, int MODE = 0>
+template <int QT, int ZM, int MODE = 0>
 __device__ __forceinline__ void ring_load(Ring<QT>& r, bool ok, const LaneAddr& la, int rq, int q) {
+  constexpr bool HAS_Z = ZM != 0, CMP = ZM == 2;  // z term; compact scales (alpha_i = 2^(i-1) s)
   if (ok) {
     const uint8_t* kp = la.kp + (size_t)rq * la.KB;
     const uint8_t* ap = la.ap + (size_t)rq * la.AB;
@@ -210,7 +210,7 @@ __device__ __forceinline__ void ring_load(Ring<QT>& r, bool ok, const LaneAddr& 
     for (int i = 0; i < QT; ++i) {
       if (QT <= 4 || i < q) {
         r.k[i] = ldg_stream_u4(kp + i * la.kstride);
-        if (MODE != 4) r.a[i] = ldg_nc_u2(ap + 8 * i);
+        if (MODE != 4 && (!CMP || i == 0)) r.a[i] = ldg_nc_u2(ap + 8 * i);
         else r.a[i] = make_uint2(0, 0);
       }
     }
@@ -226,9 +226,10 @@ __device__ __forceinline__ void ring_load(Ring<QT>& r, bool ok, const LaneAddr& 
 }
 
 // (acc01, acc23) (+)= sum_i alpha_i[r] * (LUT partial of row r, plane i) (+ z[r] * xsum)
-template <int QT, bool HAS_Z, int MODE = 0>
+template <int QT, int ZM, int MODE = 0>
 __device__ __forceinline__ void ring_compute(const Ring<QT>& r, uint32_t lc, float xsum, f32x2& acc01, f32x2& acc23,
                                              int q, bool accumulate) {
+  constexpr bool HAS_Z = ZM != 0, CMP = ZM == 2;  // z term; compact scales (alpha_i = 2^(i-1) s)
   if (MODE == 3 || MODE == 4) {  // measurement variants: consume the loaded words with minimal work
     uint32_t v = 0;
 #pragma unroll
@@ -237,9 +238,24 @@ __device__ __forceinline__ void ring_compute(const Ring<QT>& r, uint32_t lc, flo
     acc23 = pack2(0.f, 0.f);
     return;
   }
+  if (CMP) {  // P = sum_i 2^(i-1) (plane i partial) exactly scaled, then one multiply by s (App. C)
+    f32x2 p01 = 0ull, p23 = 0ull;
+#pragma unroll
+    for (int i = 0; i < QT; ++i) {
+      if (QT <= 4 || i < q) {
+        const float w2 = (float)(1 << i) * 0.5f;
+        const f32x2 ww = pack2(w2, w2);
+        p01 = fma2(ww, lut4x2<MODE>(r.k[i].x, r.k[i].y, lc), p01);
+        p23 = fma2(ww, lut4x2<MODE>(r.k[i].z, r.k[i].w, lc), p23);
+      }
+    }
+    const f32x2 s01 = h2_to_f32x2(r.a[0].x), s23 = h2_to_f32x2(r.a[0].y);
+    acc01 = accumulate ? fma2(s01, p01, acc01) : mul2(s01, p01);
+    acc23 = accumulate ? fma2(s23, p23, acc23) : mul2(s23, p23);
+  }
 #pragma unroll
   for (int i = 0; i < QT; ++i) {
-    if (QT <= 4 || i < q) {
+    if (!CMP && (QT <= 4 || i < q)) {
       const f32x2 a01 = h2_to_f32x2(r.a[i].x), a23 = h2_to_f32x2(r.a[i].y);
       const f32x2 s01 = lut4x2<MODE>(r.k[i].x, r.k[i].y, lc);
       const f32x2 s23 = lut4x2<MODE>(r.k[i].z, r.k[i].w, lc);
@@ -273,8 +289,9 @@ __device__ __forceinline__ float lane_xsum(uint32_t lut, int lane) {
 // contiguous ranges, one per CTA (a range spans at most a few slices, so a CTA
 // builds few LUTs).  Inside a range the 16 warps take row quads round-robin.
 // ---------------------------------------------------------------------------
-template <int QT, bool HAS_Z, int PD, int MODE = 0>
+template <int QT, int ZM, int PD, int MODE = 0>
 __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) {
+  constexpr bool HAS_Z = ZM != 0;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(kFull, tid >> 5, 0);  // warp-uniform for the compiler
@@ -346,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     constexpr int NB = PD + 1;
     Ring<QT> buf[NB];
     auto load_quad = [&](Ring<QT>& b, int t) {
-      ring_load<QT, HAS_Z, MODE>(b, lane_ok && t < nt, la, rq_a + warp + kWarps * t, q);
+      ring_load<QT, ZM, MODE>(b, lane_ok && t < nt, la, rq_a + warp + kWarps * t, q);
     };
 #pragma unroll
     for (int d = 0; d < PD; ++d) load_quad(buf[d], d);
@@ -382,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
           load_quad(buf[(d + PD) % NB], t + PD);
           const int rq = rq_a + warp + kWarps * t;
           f32x2 acc01, acc23;
-          ring_compute<QT, HAS_Z, MODE>(buf[d], lc, xsum, acc01, acc23, q, false);
+          ring_compute<QT, ZM, MODE>(buf[d], lc, xsum, acc01, acc23, q, false);
           const float v = reduce4(acc01, acc23, lane);
           if ((lane & 7) == 0) part[4 * rq + (lane >> 3)] = v;
         }
@@ -578,14 +595,15 @@ struct VPtr {
   uint32_t KB, AB, ZB, kstride;  // per-step strides (V quads) and the plane stride
 };
 
-template <int QT, bool HAS_Z>
+template <int QT, int ZM>
 __device__ __forceinline__ void vring_load(VRing<QT>& r, bool ok, VPtr& pt, int q) {
+  constexpr bool HAS_Z = ZM != 0, CMP = ZM == 2;  // z term; compact scales (alpha_i = 2^(i-1) s)
 #pragma unroll
   for (int i = 0; i < QT; ++i) {
     if (QT <= 4 || i < q) {
       if (ok) {
         r.k[i] = ldg_stream_u4(pt.kq + i * pt.kstride);
-        r.a[i] = ldg_nc_u2(pt.aq + 8 * i);
+        r.a[i] = (!CMP || i == 0) ? ldg_nc_u2(pt.aq + 8 * i) : make_uint2(0, 0);
       } else {
         r.k[i] = make_uint4(0, 0, 0, 0);
         r.a[i] = make_uint2(0, 0);
@@ -599,16 +617,19 @@ __device__ __forceinline__ void vring_load(VRing<QT>& r, bool ok, VPtr& pt, int 
 }
 
 // acc[rho][p] (+)= sum_i alpha_i[rho] * (word lookups of row rho, plane i) + z[rho] * xsum, rho < 4
-template <int V, int QT, bool HAS_Z>
+template <int V, int QT, int ZM>
 __device__ __forceinline__ void vring_compute(const VRing<QT>& r, uint32_t lc, const f32x2 (&xs)[V / 2],
                                               f32x2 (&acc)[4][V / 2], int q) {
+  constexpr bool HAS_Z = ZM != 0, CMP = ZM == 2;  // z term; compact scales (alpha_i = 2^(i-1) s)
   constexpr int NP = V / 2;
+  f32x2 P[4][NP];  // compact: sum_i 2^(i-1) (plane i lookups), scaled by s after the planes
 #pragma unroll
   for (int i = 0; i < QT; ++i) {
     if (QT <= 4 || i < q) {
       const uint32_t kw[4] = {r.k[i].x, r.k[i].y, r.k[i].z, r.k[i].w};
       const float2 a01 = h2_to_f2(r.a[i].x), a23 = h2_to_f2(r.a[i].y);
-      const float al[4] = {a01.x, a01.y, a23.x, a23.y};
+      const float w2 = (float)(1 << i) * 0.5f;
+      const float al[4] = {CMP ? w2 : a01.x, CMP ? w2 : a01.y, CMP ? w2 : a23.x, CMP ? w2 : a23.y};
       // all 16 lookups of the plane are issued before the first add (ILP over
       // the LDS latency), then summed per row and scaled
       f32x2 t[4][4][NP];
@@ -625,10 +646,19 @@ __device__ __forceinline__ void vring_compute(const VRing<QT>& r, uint32_t lc, c
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
           const f32x2 s = add2(add2(t[rho][0][p], t[rho][1][p]), add2(t[rho][2][p], t[rho][3][p]));
-          acc[rho][p] = fma2(aa, s, acc[rho][p]);
+          if (!CMP) acc[rho][p] = fma2(aa, s, acc[rho][p]);
+          else P[rho][p] = i == 0 ? mul2(aa, s) : fma2(aa, s, P[rho][p]);
         }
       }
     }
+  }
+  if (CMP) {
+    const float2 s01 = h2_to_f2(r.a[0].x), s23 = h2_to_f2(r.a[0].y);
+    const float sv[4] = {s01.x, s01.y, s23.x, s23.y};
+#pragma unroll
+    for (int rho = 0; rho < 4; ++rho)
+#pragma unroll
+      for (int p = 0; p < NP; ++p) acc[rho][p] = fma2(pack2(sv[rho], sv[rho]), P[rho][p], acc[rho][p]);
   }
   if (HAS_Z) {
     const float2 z01 = h2_to_f2(r.z.x), z23 = h2_to_f2(r.z.y);
@@ -652,8 +682,9 @@ struct VStep {
 // Lanes: lane = qi * LR + wv: quad qi of each group of V consecutive quads
 // (all 4 rows of it), wv = w * NV + v as above.  A warp owns QPW consecutive
 // quads of the work item's row block, processed as QPW / V steps.
-template <int V, int QT, bool HAS_Z, int PD, int QPW, int NTH>
+template <int V, int QT, int ZM, int PD, int QPW, int NTH>
 __global__ void __launch_bounds__(NTH, 1) lut_gemm_batched_kernel(const KParams p) {
+  constexpr bool HAS_Z = ZM != 0;
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int LR = 32 / V, NP = V / 2, NB = PD + 1, NT = QPW / V;
   static_assert(QPW % V == 0 && NT % NB == 0, "the ring restarts at buffer 0 every sub-slice");
@@ -722,7 +753,7 @@ __global__ void __launch_bounds__(NTH, 1) lut_gemm_batched_kernel(const KParams 
     pt.ZB = ZB * V;
     pt.kstride = (uint32_t)Ls * 16u;
     pt.kq = p.data + keys_base(sh, st.s, Ls) + (size_t)rq * KB + pl * 16;
-    pt.aq = p.data + alpha_base(sh, st.s, Ls) + (size_t)rq * AB + (uint32_t)(pl >> gsh) * sh.q * 8u;
+    pt.aq = p.data + alpha_base(sh, st.s, Ls) + (size_t)rq * AB + (uint32_t)(pl >> gsh) * scale_planes(sh) * 8u;
     pt.zq = p.data + z_base(sh, st.s, Ls) + (size_t)rq * ZB + (uint32_t)(pl >> gsh) * 8u;
     return pt;
   };
@@ -733,7 +764,7 @@ __global__ void __launch_bounds__(NTH, 1) lut_gemm_batched_kernel(const KParams 
     const int rq_w = (st.it % NRB) * rbq + warp * QPW;
     nxt = lane_ptr(st, rq_w, nxt_ok);
 #pragma unroll
-    for (int d = 0; d < PD; ++d) vring_load<QT, HAS_Z>(ring[d], nxt_ok && rq_w + V * d + qi < sh.RQ, nxt, q);
+    for (int d = 0; d < PD; ++d) vring_load<QT, ZM>(ring[d], nxt_ok && rq_w + V * d + qi < sh.RQ, nxt, q);
   };
 
   VStep st = first_step(it0);
@@ -767,8 +798,8 @@ __global__ void __launch_bounds__(NTH, 1) lut_gemm_batched_kernel(const KParams 
       if (HAS_Z) vword<V>(0xFFFFFFFFu, lc, xs);  // sum of x over the lane's 32 columns = sum_J T_J[255]
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
-        if (t + PD < NT) vring_load<QT, HAS_Z>(ring[(t + PD) % NB], lane_ok && V * (t + PD) < nql, cur, q);
-        vring_compute<V, QT, HAS_Z>(ring[t % NB], lc, xs, acc[t], q);
+        if (t + PD < NT) vring_load<QT, ZM>(ring[(t + PD) % NB], lane_ok && V * (t + PD) < nql, cur, q);
+        vring_compute<V, QT, ZM>(ring[t % NB], lc, xs, acc[t], q);
       }
       if (sn.it < it1) prologue(sn);  // next step's first quads fly during the barrier and rebuild
       cp_async_wait_all();
@@ -930,45 +961,45 @@ static cudaError_t launch_reduce(const KParams& p, cudaStream_t st) {
                             p.yf, p.counters);
 }
 
-template <int QT, bool HAS_Z>
+template <int QT, int ZM>
 static cudaError_t launch_gemv_t(const KParams& p, int grid, cudaStream_t st) {
   // quads in flight per warp while one is computed (ring of PD + 1 buffers)
   constexpr int PD = QT <= 1 ? 6 : (QT <= 2 ? 4 : (QT <= 4 ? 2 : 1));
-  if constexpr (QT == 3 && !HAS_Z) {
+  if constexpr (QT == 3 && ZM == 0) {
     if (p.xmode >= 10) {  // measurement variants (LUTGEMM_XMODE)
     switch (p.xmode) {
-      case 10: return launch(lut_gemv_kernel<QT, HAS_Z, 1, 0>, grid, p, st);
-      case 11: return launch(lut_gemv_kernel<QT, HAS_Z, 2, 1>, grid, p, st);
-      case 13: return launch(lut_gemv_kernel<QT, HAS_Z, 2, 3>, grid, p, st);
-      case 16: return launch(lut_gemv_kernel<QT, HAS_Z, 2, 4>, grid, p, st);
-      case 14: return launch(lut_gemv_kernel<QT, HAS_Z, 3, 0>, grid, p, st);
-      case 18: return launch(lut_gemv_kernel<QT, HAS_Z, 4, 0>, grid, p, st);
+      case 10: return launch(lut_gemv_kernel<QT, ZM, 1, 0>, grid, p, st);
+      case 11: return launch(lut_gemv_kernel<QT, ZM, 2, 1>, grid, p, st);
+      case 13: return launch(lut_gemv_kernel<QT, ZM, 2, 3>, grid, p, st);
+      case 16: return launch(lut_gemv_kernel<QT, ZM, 2, 4>, grid, p, st);
+      case 14: return launch(lut_gemv_kernel<QT, ZM, 3, 0>, grid, p, st);
+      case 18: return launch(lut_gemv_kernel<QT, ZM, 4, 0>, grid, p, st);
       default: break;
     }
     }
   }
-  return launch(lut_gemv_kernel<QT, HAS_Z, PD>, grid, p, st);
+  return launch(lut_gemv_kernel<QT, ZM, PD>, grid, p, st);
 }
 
 // batched: V-wide slots (V = 2 only for b = 2); p.qpw = row quads per work item
 // (256 or 128).  V = 2 runs 16 warps (128 registers: 4 rows x 2 batch x 16
 // quads of accumulators), V = 4 and q > 4 run 8 warps (255 registers).
-template <int V, int QT, bool HAS_Z>
+template <int V, int QT, int ZM>
 static cudaError_t launch_batched_v(const KParams& p, int grid, cudaStream_t st) {
   if constexpr (QT <= 4 && V == 2) {
-    if (p.qpw == 128) return launch(lut_gemm_batched_kernel<V, QT, HAS_Z, 1, 8, 512>, grid, p, st, 512);
-    return launch(lut_gemm_batched_kernel<V, QT, HAS_Z, 1, 16, 512>, grid, p, st, 512);
+    if (p.qpw == 128) return launch(lut_gemm_batched_kernel<V, QT, ZM, 1, 8, 512>, grid, p, st, 512);
+    return launch(lut_gemm_batched_kernel<V, QT, ZM, 1, 16, 512>, grid, p, st, 512);
   } else if constexpr (QT <= 4) {
-    if (p.qpw == 128) return launch(lut_gemm_batched_kernel<V, QT, HAS_Z, 1, 16, 256>, grid, p, st, 256);
-    return launch(lut_gemm_batched_kernel<V, QT, HAS_Z, 1, 32, 256>, grid, p, st, 256);
+    if (p.qpw == 128) return launch(lut_gemm_batched_kernel<V, QT, ZM, 1, 16, 256>, grid, p, st, 256);
+    return launch(lut_gemm_batched_kernel<V, QT, ZM, 1, 32, 256>, grid, p, st, 256);
   } else {
-    return launch(lut_gemm_batched_kernel<V, QT, HAS_Z, 1, 16, 256>, grid, p, st, 256);
+    return launch(lut_gemm_batched_kernel<V, QT, ZM, 1, 16, 256>, grid, p, st, 256);
   }
 }
 
-template <int QT, bool HAS_Z>
+template <int QT, int ZM>
 static cudaError_t launch_batched_t(const KParams& p, int grid, cudaStream_t st) {
-  return p.b == 2 ? launch_batched_v<2, QT, HAS_Z>(p, grid, st) : launch_batched_v<4, QT, HAS_Z>(p, grid, st);
+  return p.b == 2 ? launch_batched_v<2, QT, ZM>(p, grid, st) : launch_batched_v<4, QT, ZM>(p, grid, st);
 }
 
 static cudaError_t launch_reduce_batched(const KParams& p, cudaStream_t st) {
@@ -1012,14 +1043,14 @@ static void plan_batched(const Shape& sh, int sms, KParams& p) {
   }
 }
 
-template <bool HAS_Z>
+template <int ZM>
 static cudaError_t dispatch_q(const KParams& p, int grid, cudaStream_t st, bool batched) {
   switch (p.sh.q) {
-    case 1: return batched ? launch_batched_t<1, HAS_Z>(p, grid, st) : launch_gemv_t<1, HAS_Z>(p, grid, st);
-    case 2: return batched ? launch_batched_t<2, HAS_Z>(p, grid, st) : launch_gemv_t<2, HAS_Z>(p, grid, st);
-    case 3: return batched ? launch_batched_t<3, HAS_Z>(p, grid, st) : launch_gemv_t<3, HAS_Z>(p, grid, st);
-    case 4: return batched ? launch_batched_t<4, HAS_Z>(p, grid, st) : launch_gemv_t<4, HAS_Z>(p, grid, st);
-    default: return batched ? launch_batched_t<8, HAS_Z>(p, grid, st) : launch_gemv_t<8, HAS_Z>(p, grid, st);
+    case 1: return batched ? launch_batched_t<1, ZM>(p, grid, st) : launch_gemv_t<1, ZM>(p, grid, st);
+    case 2: return batched ? launch_batched_t<2, ZM>(p, grid, st) : launch_gemv_t<2, ZM>(p, grid, st);
+    case 3: return batched ? launch_batched_t<3, ZM>(p, grid, st) : launch_gemv_t<3, ZM>(p, grid, st);
+    case 4: return batched ? launch_batched_t<4, ZM>(p, grid, st) : launch_gemv_t<4, ZM>(p, grid, st);
+    default: return batched ? launch_batched_t<8, ZM>(p, grid, st) : launch_gemv_t<8, ZM>(p, grid, st);
   }
 }
 
@@ -1116,7 +1147,8 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
       grid = sh.S * J;
     }
   }
-  cudaError_t e = sh.has_z ? dispatch_q<true>(p, grid, st, batched) : dispatch_q<false>(p, grid, st, batched);
+  cudaError_t e = sh.compact ? dispatch_q<2>(p, grid, st, batched)
+                             : (sh.has_z ? dispatch_q<1>(p, grid, st, batched) : dispatch_q<0>(p, grid, st, batched));
   if (e != cudaSuccess) return e;
   if (p.fused_J > 0) return cudaSuccess;  // reduced in-kernel
   if (p.xmode == 2) return cudaSuccess;  // experiment: no reduction (wrong results, timing only)

@@ -5,7 +5,7 @@
 // UNIFORM source: App. C -- plane i bit = bit i of the code
 // (b_i = 2 b_hat_i - 1), alpha_i = 2^(i-1) s (exact power-of-two
 // scaling of an fp16 s), z = sum_i alpha_i + z_hat summed in fp64 and rounded
-// once to fp16 (R17).  Offline and untimed ("two-step methodology").
+// once to fp16 (R17).  The compact format stores s instead of the q alphas.  Offline and untimed ("two-step methodology").
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -97,9 +97,14 @@ __global__ void unpack_scales_kernel(const uint8_t* __restrict__ src, uint16_t* 
     int s, k;
     home_of_group(sh, grp, &s, &k);
     const int Ls = slice_lanes(sh.n, s);
-    if (alpha)
+    if (alpha && sh.compact) {  // alpha_i = 2^(i-1) s
+      const double sv = (double)__half2float(
+          __ushort_as_half(*reinterpret_cast<const uint16_t*>(src + alpha_at(sh, s, Ls, r / 4, 0, k, r % 4))));
+      for (int i = 0; i < sh.q; ++i) alpha[idx * sh.q + i] = __half_as_ushort(__double2half(ldexp(sv, i - 1)));
+    } else if (alpha) {
       for (int i = 0; i < sh.q; ++i)
         alpha[idx * sh.q + i] = *reinterpret_cast<const uint16_t*>(src + alpha_at(sh, s, Ls, r / 4, i, k, r % 4));
+    }
     if (offset && sh.has_z)
       offset[idx] = *reinterpret_cast<const uint16_t*>(src + z_at(sh, s, Ls, r / 4, k, r % 4));
   }
@@ -149,8 +154,12 @@ __global__ void pack_uniform_scales_kernel(const uint16_t* __restrict__ scale, c
       for (int i = 0; i < sh.q; ++i) {
         const double a = ldexp(sv, i - 1);
         sum_alpha += a;
-        *reinterpret_cast<uint16_t*>(dst + alpha_at(sh, s, Ls, rq, i, k, r4)) = __half_as_ushort(__double2half(a));
+        if (!sh.compact)
+          *reinterpret_cast<uint16_t*>(dst + alpha_at(sh, s, Ls, rq, i, k, r4)) = __half_as_ushort(__double2half(a));
       }
+      if (sh.compact)  // the compact format stores s itself (alpha_i = 2^(i-1) s derived in-kernel)
+        *reinterpret_cast<uint16_t*>(dst + alpha_at(sh, s, Ls, rq, 0, k, r4)) =
+            r < sh.m ? scale[(size_t)r * sh.G + grp] : (uint16_t)0;
       *reinterpret_cast<uint16_t*>(dst + z_at(sh, s, Ls, rq, k, r4)) =
           __half_as_ushort(__double2half(r < sh.m ? sum_alpha + zh : 0.0));
     }

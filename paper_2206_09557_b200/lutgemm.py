@@ -18,7 +18,8 @@ LIB_PATH = os.path.join(_HERE, "liblutgemm.so")
 
 OK = 0
 STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "MISALIGNED", 3: "WORKSPACE", 4: "CUDA", 5: "NCCL", 6: "UNSUPPORTED"}
-SRC_BCQ, SRC_UNIFORM = 0, 1
+SRC_BCQ, SRC_UNIFORM, SRC_UNIFORM_COMPACT = 0, 1, 2
+FMT_BCQ, FMT_UNIFORM_COMPACT = 0, 1
 TP_ROWS_LOCAL, TP_ROWS_ALLGATHER, TP_COLS_ALLREDUCE = 0, 1, 2
 
 
@@ -30,7 +31,7 @@ class LutgemmError(RuntimeError):
 
 class lutgemm_weight(ctypes.Structure):
     _fields_ = [("m", ctypes.c_int32), ("n", ctypes.c_int32), ("q", ctypes.c_int32), ("g", ctypes.c_int32),
-                ("has_offset", ctypes.c_int32), ("reserved", ctypes.c_int32), ("data", ctypes.c_void_p)]
+                ("has_offset", ctypes.c_int32), ("format", ctypes.c_int32), ("data", ctypes.c_void_p)]
 
 
 class lutgemm_pack_src(ctypes.Structure):
@@ -48,6 +49,7 @@ SIGNATURES = [
     ("lutgemm_abi_version", _I, []),
     ("lutgemm_last_error", ctypes.c_char_p, []),
     ("lutgemm_packed_bytes", _I, [_I, _I, _I, _I, _I, ctypes.POINTER(_SZ)]),
+    ("lutgemm_packed_bytes_fmt", _I, [_I, _I, _I, _I, _I, _I, ctypes.POINTER(_SZ)]),
     ("lutgemm_pack_bcq", _I, [ctypes.POINTER(lutgemm_pack_src), ctypes.POINTER(lutgemm_weight), _P]),
     ("lutgemm_unpack_bcq", _I, [ctypes.POINTER(lutgemm_weight), _P, _P, _P, _P]),
     ("lutgemm_workspace_bytes", _SZ, [_I, _I, _I]),
@@ -98,9 +100,10 @@ def _stream(stream=None) -> int:
     return s.cuda_stream
 
 
-def lutgemm_packed_bytes(m: int, n: int, q: int, g: int, has_offset: bool) -> int:
+def lutgemm_packed_bytes(m: int, n: int, q: int, g: int, has_offset: bool, fmt: int = FMT_BCQ) -> int:
     a = _SZ()
-    _check("lutgemm_packed_bytes", lib.lutgemm_packed_bytes(m, n, q, g, int(has_offset), ctypes.byref(a)))
+    _check("lutgemm_packed_bytes_fmt",
+           lib.lutgemm_packed_bytes_fmt(m, n, q, g, int(has_offset), int(fmt), ctypes.byref(a)))
     return a.value
 
 
@@ -115,12 +118,13 @@ class PackedBCQ:
     has_offset: bool
     data: torch.Tensor
     struct: lutgemm_weight = field(default=None)
+    fmt: int = FMT_BCQ
 
     @classmethod
-    def empty(cls, m, n, q, g, has_offset, device) -> "PackedBCQ":
-        data = torch.empty(lutgemm_packed_bytes(m, n, q, g, has_offset), dtype=torch.uint8, device=device)
-        w = cls(m, n, q, g, has_offset, data)
-        w.struct = lutgemm_weight(m, n, q, g, int(has_offset), 0, data.data_ptr())
+    def empty(cls, m, n, q, g, has_offset, device, fmt: int = FMT_BCQ) -> "PackedBCQ":
+        data = torch.empty(lutgemm_packed_bytes(m, n, q, g, has_offset, fmt), dtype=torch.uint8, device=device)
+        w = cls(m, n, q, g, has_offset, data, fmt=fmt)
+        w.struct = lutgemm_weight(m, n, q, g, int(has_offset), int(fmt), data.data_ptr())
         return w
 
     def nbytes(self) -> int:
@@ -143,15 +147,17 @@ def lutgemm_pack_bcq(planes: torch.Tensor, alpha: torch.Tensor, offset: torch.Te
 
 
 def lutgemm_pack_uniform(codes: torch.Tensor, scale: torch.Tensor, zero: torch.Tensor, q: int, g: int,
-                         stream=None) -> PackedBCQ:
-    """Uniform codes (uint8 [m][n]), s and z_hat (fp16 [m][n/g]) -> extended BCQ (App. C)."""
+                         stream=None, compact: bool = False) -> PackedBCQ:
+    """Uniform codes (uint8 [m][n]), s and z_hat (fp16 [m][n/g]) -> extended BCQ (App. C).
+    compact=True keeps one scale s per group (format UNIFORM_COMPACT, alpha_i derived in-kernel)."""
     m, n = int(codes.shape[0]), int(codes.shape[1])
     for t in (codes, scale, zero):
         if not t.is_cuda or not t.is_contiguous():
             raise ValueError("pack sources must be contiguous CUDA tensors")
-    w = PackedBCQ.empty(m, n, q, g, True, codes.device)
-    src = lutgemm_pack_src(SRC_UNIFORM, m, n, q, g, 0, None, None, None, codes.data_ptr(), scale.data_ptr(),
-                           zero.data_ptr())
+    fmt = FMT_UNIFORM_COMPACT if compact else FMT_BCQ
+    w = PackedBCQ.empty(m, n, q, g, True, codes.device, fmt)
+    src = lutgemm_pack_src(SRC_UNIFORM_COMPACT if compact else SRC_UNIFORM, m, n, q, g, 0, None, None, None,
+                           codes.data_ptr(), scale.data_ptr(), zero.data_ptr())
     _check("lutgemm_pack_bcq", lib.lutgemm_pack_bcq(ctypes.byref(src), ctypes.byref(w.struct), _stream(stream)))
     return w
 

@@ -58,12 +58,17 @@ def test_unpack_round_trip_bit_exact(m, n, q, g, off):
 
 @pytest.mark.parametrize("m,n,q,g", [(8, 64, 1, 32), (33, 256, 2, 64), (64, 512, 3, 128), (100, 1536, 4, 128),
                                      (17, 1024, 8, 256)])
-def test_uniform_pack_matches_oracle_conversion(m, n, q, g):
+@pytest.mark.parametrize("compact", [False, True])
+def test_uniform_pack_matches_oracle_conversion(m, n, q, g, compact):
     """GPU App. C conversion == oracle.uniform_to_bcq followed by the fp16
-    storage step, bit for bit (planes, alpha, z)."""
+    storage step, bit for bit (planes, alpha, z).  The compact format stores s
+    and unpacks to alpha_i = 2^(i-1) s: the same canonical bytes."""
     import paper_2206_09557_b200 as L
     u = gen_uniform(m * n + q, m, n, q, g)
-    w = L.lutgemm_pack_uniform(dev(u["codes"]), dev(u["scale"]), dev(u["zero"]), q, g)
+    w = L.lutgemm_pack_uniform(dev(u["codes"]), dev(u["scale"]), dev(u["zero"]), q, g, compact=compact)
+    if compact:  # one fp16 scale per (row, group) instead of q
+        assert w.nbytes() < L.lutgemm_packed_bytes(m, n, q, g, True) or q == 1
+        assert w.fmt == L.FMT_UNIFORM_COMPACT
     p, a, z = L.lutgemm_unpack_bcq(w)
     torch.cuda.synchronize()
     planes, alpha, zz = O.uniform_to_bcq(u["codes"], u["scale"], u["zero"], q)

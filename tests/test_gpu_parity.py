@@ -180,14 +180,16 @@ def test_attention_qg_grid_sampled(q, g):
     assert_parity(y[rows], O.bcq_gemv_rows(d["planes"], d["alpha"], None, X, n, g, rows)[0], (q, g))
 
 
+@pytest.mark.parametrize("compact", [False, True])
 @pytest.mark.parametrize("name", ["llama_sq", "llama_up", "llama_down"])
-def test_llama_uniform_sampled(name):
-    """Config 4: uniform 4-bit codes converted to BCQ with offset (App. C)."""
+def test_llama_uniform_sampled(name, compact):
+    """Config 4: uniform 4-bit codes converted to BCQ with offset (App. C);
+    compact: one stored s per group, alpha_i = 2^(i-1) s derived in-kernel."""
     import paper_2206_09557_b200 as L
     c = CONFIGS[name]
     u = gen_uniform(c["seed"], c["m"], c["n"], c["q"], c["g"])
     X = gen_x(c["seed"], 1, c["n"])
-    w = L.lutgemm_pack_uniform(dev(u["codes"]), dev(u["scale"]), dev(u["zero"]), c["q"], c["g"])
+    w = L.lutgemm_pack_uniform(dev(u["codes"]), dev(u["scale"]), dev(u["zero"]), c["q"], c["g"], compact=compact)
     y = run(w, X)[0]
     rows = _sampled_rows(c["m"], c["seed"], k=128)
     planes, alpha, z = O.uniform_to_bcq(u["codes"][rows], u["scale"][rows], u["zero"][rows], c["q"])
@@ -239,3 +241,26 @@ def test_error_paths_on_device():
     with pytest.raises(L.LutgemmError) as ei:
         L.lutgemm_gemv(w, x[:256], ws=ws)
     assert ei.value.status == 3
+
+
+@pytest.mark.parametrize("b", [1, 2, 4, 7, 32])
+@pytest.mark.parametrize("m,n,q,g", [(333, 1536, 3, 128), (1030, 5152, 4, 32), (64, 2048, 2, 2048), (40, 1024, 6, 64)])
+def test_uniform_compact_full_parity(b, m, n, q, g):
+    """Compact uniform format vs the fp64 oracle of the App. C
+    conversion with the fp16-stored z (R17), GEMV and batched; and against the
+    expanded (q alphas) packing of the same source within rounding."""
+    import paper_2206_09557_b200 as L
+    u = gen_uniform(m + n + q + b, m, n, q, g)
+    X = gen_x(m + b, b, n)
+    src = (dev(u["codes"]), dev(u["scale"]), dev(u["zero"]))
+    wc = L.lutgemm_pack_uniform(*src, q, g, compact=True)
+    we = L.lutgemm_pack_uniform(*src, q, g)
+    planes, alpha, z = O.uniform_to_bcq(u["codes"], u["scale"], u["zero"], q)
+    ref = O.bcq_gemv(planes, O.store_fp16(alpha), O.store_fp16(z), X, n, g)
+    yc = run(wc, X)
+    assert_parity(yc, ref, ("compact", b, m, n, q, g))
+    assert parity(yc.ravel(), run(we, X).ravel())["rel_l2"] <= 1e-3
+    # bitwise reproducible and exact under x -> 2x
+    yf = run(wc, X, f32=True)
+    assert np.array_equal(run(wc, X, f32=True), yf)
+    assert np.array_equal(run(wc, (2 * X.astype(np.float32)).astype(np.float16), f32=True), 2 * yf)

@@ -63,16 +63,16 @@ def time_product(ws_list, X, b, m, n, steps):
     return a.elapsed_time(e) / (reps * G) * 1e3  # us per product
 
 
-def case(name, m, n, q, g, b=1, uniform=False, steps=400, seed=7):
+def case(name, m, n, q, g, b=1, uniform=False, steps=400, seed=7, compact=False):
     dev = torch.device("cuda")
     offset = uniform
-    B = algorithmic_bytes(m, n, q, g, b, offset)
+    B = algorithmic_bytes(m, n, q, g, b, offset, compact)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     ncopies = max(2, math.ceil(3 * l2 / B))
     if uniform:
         u = gen_uniform(seed, m, n, q, g)
         codes, s, z = (torch.from_numpy(u[k]).to(dev) for k in ("codes", "scale", "zero"))
-        ws_list = [L.lutgemm_pack_uniform(codes, s, z, q, g) for _ in range(ncopies)]
+        ws_list = [L.lutgemm_pack_uniform(codes, s, z, q, g, compact=compact) for _ in range(ncopies)]
     else:
         d = gen_bcq(seed, m, n, q, g)
         planes = torch.from_numpy(d["planes"].view(np.int32)).to(dev)
@@ -85,7 +85,8 @@ def case(name, m, n, q, g, b=1, uniform=False, steps=400, seed=7):
     lookups = m * q * (n // 8) * b
     lds_us = lookups / 32 / torch.cuda.get_device_properties(dev).multi_processor_count / SM_HZ * 1e6
     hbm_us = B / (peak * 1e9) * 1e6
-    out = {"case": name, "m": m, "n": n, "q": q, "g": g, "b": b, "offset": offset, "us": round(us, 3),
+    out = {"case": name, "m": m, "n": n, "q": q, "g": g, "b": b, "offset": offset, "compact": compact,
+           "us": round(us, 3),
            "GBps": round(gbs, 1), "frac_hbm": round(gbs / peak, 4), "bytes_alg": B,
            "hbm_roof_us": round(hbm_us, 2), "lds_roof_us": round(lds_us, 2),
            "bound": "hbm" if hbm_us >= lds_us else "lds",
@@ -107,7 +108,9 @@ def main():
             f = [int(v) for v in c.split(":")]
             m, n, q, g = f[:4]
             b = f[4] if len(f) > 4 else 1
-            case(f"{m}x{n}_q{q}_g{g}_b{b}", m, n, q, g, b=b, uniform=len(f) > 5 and f[5] == 1, steps=args.steps)
+            u = f[5] if len(f) > 5 else 0  # 1: uniform (App. C), 2: uniform compact format
+            case(f"{m}x{n}_q{q}_g{g}_b{b}" + ("_c" if u == 2 else ""), m, n, q, g, b=b, uniform=u >= 1,
+                 steps=args.steps, compact=u == 2)
         return
     only = set(args.only.split(","))
     if "ffn" in only:
@@ -121,6 +124,9 @@ def main():
         case("llama_8192x8192", 8192, 8192, 4, 128, uniform=True, steps=args.steps)
         case("llama_up_22016x8192", 22016, 8192, 4, 128, uniform=True, steps=args.steps)
         case("llama_down_8192x22016", 8192, 22016, 4, 128, uniform=True, steps=args.steps)
+        case("llama_8192x8192_compact", 8192, 8192, 4, 128, uniform=True, steps=args.steps, compact=True)
+        case("llama_up_22016x8192_compact", 22016, 8192, 4, 128, uniform=True, steps=args.steps, compact=True)
+        case("llama_down_8192x22016_compact", 8192, 22016, 4, 128, uniform=True, steps=args.steps, compact=True)
     if "batched" in only:
         for b in (2, 4, 8, 16, 32):
             case(f"fc1_b{b}", 49152, 12288, 3, 128, b=b, steps=max(20, args.steps // (4 * b)))
