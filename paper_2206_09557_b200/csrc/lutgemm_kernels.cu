@@ -323,6 +323,11 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
   const uint32_t lc = (sm.lut & 0xFFFF0000u) | ((uint32_t)(4 * lane + 128) << 8) | (uint32_t)(4 * lane);
   const int pf_steps = p.pf_steps;
 
+  // last-arriver reduction (p.last_red): the next kernel may launch right away;
+  // its CTAs take SMs as soon as this grid's CTAs exit and stream their first
+  // weights before their own PDL wait
+  const bool last_red = J > 0 && p.last_red;
+  if (last_red) pdl_launch_dependents();
   if (tid == 0) {
     mbar_init(bar0, 1);
     mbar_init(bar1, 1);
@@ -345,16 +350,6 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     //    preceding kernel until it completes) is requested before anything
     //    else, so it is not queued behind the weight stream; then an L2
     //    prefetch of the first weight steps and the register ring
-    if (e == 0) {
-      // weights of the steps after the register prologue into L2 while the
-      // preceding kernel drains (a plain prefetch: legal before the PDL wait)
-      if (tid == 0 && p.pf_init > PD)
-        prefetch_quads(sh, p.data, s, Ls, min(rq_b, rq_a + PD * kWarps), min(rq_b, rq_a + p.pf_init * kWarps));
-      pdl_wait();
-      if (trace) trace[5] = globaltimer_ns();
-      if (warp == 0) stage_x(xbuf0, bar0, p.x, sh.n, s * kSliceCols, Ls, 32, 1, 1, lane);
-    }
-    if (tid == 0 && pf_steps > 0) prefetch_quads(sh, p.data, s, Ls, rq_a, min(rq_b, rq_a + pf_steps * kWarps));
     // this warp's row quads in the segment: rq_a + warp + 16 t, t < nt
     const int nt = rq_a + warp < rq_b ? (rq_b - (rq_a + warp) + kWarps - 1) / kWarps : 0;
     // a ring of NB = PD + 1 single-quad buffers: the load for quad t + PD is
@@ -365,8 +360,25 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     auto load_quad = [&](Ring<QT>& b, int t) {
       ring_load<QT, ZM, MODE>(b, lane_ok && t < nt, la, rq_a + warp + kWarps * t, q);
     };
+    const bool early = e == 0 && last_red && p.last_red == 1;
+    if (early) {  // weights only: legal before the PDL wait
 #pragma unroll
-    for (int d = 0; d < PD; ++d) load_quad(buf[d], d);
+      for (int d = 0; d < PD; ++d) load_quad(buf[d], d);
+    }
+    if (e == 0) {
+      // weights of the steps after the register prologue into L2 while the
+      // preceding kernel drains (a plain prefetch: legal before the PDL wait)
+      if (tid == 0 && p.pf_init > PD)
+        prefetch_quads(sh, p.data, s, Ls, min(rq_b, rq_a + PD * kWarps), min(rq_b, rq_a + p.pf_init * kWarps));
+      pdl_wait();
+      if (trace) trace[5] = globaltimer_ns();
+      if (warp == 0) stage_x(xbuf0, bar0, p.x, sh.n, s * kSliceCols, Ls, 32, 1, 1, lane);
+    }
+    if (tid == 0 && pf_steps > 0) prefetch_quads(sh, p.data, s, Ls, rq_a, min(rq_b, rq_a + pf_steps * kWarps));
+    if (!early) {
+#pragma unroll
+      for (int d = 0; d < PD; ++d) load_quad(buf[d], d);
+    }
     if (e == 0) __syncthreads();  // the zero-fill of the x buffer is visible
     // 2. wait for the staged x slice and build the 128 LUTs of the slice
     __half* xb = (e & 1) ? xbuf1 : xbuf0;
@@ -406,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
       }
     }
     if (trace && e == 0) trace[3] = globaltimer_ns();  // warp 0's loop end
-    if (J > 0) {  // fused mode: each warp publishes its partials with one release increment
+    if (J > 0 && !last_red) {  // fused mode: each warp publishes its partials with one release increment
       __syncwarp();
       if (lane == 0) red_release_add_u32(p.counters + blockIdx.x % J, 1u);
     }
@@ -416,6 +428,43 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     ++e;
   }
   if (trace) trace[7] |= (unsigned long long)e << 32;  // segments processed
+  if (last_red) {
+    // The S CTAs of row-quad group fj count in; the last one to arrive sums the
+    // group's rows over the S slices in slice order (deterministic, R11); the
+    // others exit at once, freeing their SM for the next kernel.
+    __shared__ unsigned s_last;
+    const int fj = blockIdx.x % J;
+    if (e == 0) pdl_wait();  // an empty range never waited: the counters belong to the preceding kernel
+    __syncthreads();         // all partial stores of this CTA are issued
+    if (tid == 0) {
+      __threadfence();
+      const unsigned old = atomicAdd(p.counters + fj, 1u);
+      s_last = old == (unsigned)sh.S - 1;
+      if (s_last) __threadfence();
+    }
+    __syncthreads();
+    if (!s_last) return;
+    if (trace) trace[5] = globaltimer_ns();
+    const int r0 = 4 * (int)((long long)sh.RQ * fj / J);
+    const int r1 = min(sh.m, 4 * (int)((long long)sh.RQ * (fj + 1) / J));
+    for (int r = r0 + tid; r < r1; r += kThreads) {
+      float v = 0.f;
+      const float* pp = p.partial + r;
+      for (int ss0 = 0; ss0 < sh.S; ss0 += 16) {
+        float t[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) t[k] = (ss0 + k < sh.S) ? __ldcg(pp + (size_t)(ss0 + k) * sh.m4) : 0.f;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if (ss0 + k < sh.S) v += t[k];
+      }
+      if (p.yf) p.yf[r] = v;
+      else p.y[r] = __float2half_rn(v);
+    }
+    if (tid == 0) p.counters[fj] = 0u;
+    if (trace) trace[6] = globaltimer_ns();
+    return;
+  }
   if (J > 0) {
     // Fused cross-slice reduction: the S CTAs that share row-quad group fj
     // (one per slice) meet at a counter -- all CTAs of the grid are resident
@@ -1139,12 +1188,21 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
   // fused mode (b = 1): whole slices per CTA group, S*J CTAs with J per slice,
   // when that idles at most 8 % of the SMs; the reduction then runs in-kernel
   p.fused_J = 0;
+  p.last_red = 0;
   if (!batched && p.xmode != 4) {
     const int sms = num_sms();
     const int J = sh.S <= sms ? sms / sh.S : 0;
     if (J >= 1 && J <= kFusedMaxJ && sh.S <= kFusedMaxJ && sh.S * J * 100 >= sms * 92 && sh.RQ >= J) {
       p.fused_J = J;
       grid = sh.S * J;
+      // small reductions (<= 64 KB of partials per row-quad group): the last CTA
+      // of a group reduces it alone and the others exit early (the next kernel
+      // starts streaming on their SMs); large ones keep the parallel group barrier
+      const long long red_bytes = (long long)sh.S * 16 * ((sh.RQ + J - 1) / J);
+      p.last_red = red_bytes <= 65536 ? 1 : 0;
+      if (p.xmode == 40) p.last_red = 1;
+      if (p.xmode == 41) p.last_red = 2;
+      if (p.xmode == 42) p.last_red = 0;
     }
   }
   cudaError_t e = sh.compact ? dispatch_q<2>(p, grid, st, batched)
