@@ -28,8 +28,8 @@ struct KParams {
   int pf_init;       // GEMV: 16-quad steps bulk-prefetched into L2 before the PDL wait
   int xmode;         // experiment knob (0 default)
   int fused_J;       // GEMV: CTAs per slice in the fused-reduction mode (0: separate reduction kernel)
-  int last_red;      // GEMV fused mode: 1 = last-arriving CTA of a group reduces, early PDL trigger + weights before
-                     //   the PDL wait; 2 = the same without the early weight loads; 0 = group barrier
+  int last_red;      // GEMV fused mode: R > 0 = the last R CTAs to arrive in a row-quad group reduce it, the others
+                     //   exit early (early PDL trigger, weights streamed before the PDL wait); 0 = group barrier
   long long items;
   unsigned long long* trace;  // optional per-CTA timeline (kTraceSlots u64 per CTA), or null
 };

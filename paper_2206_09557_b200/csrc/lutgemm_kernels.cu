@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     auto load_quad = [&](Ring<QT>& b, int t) {
       ring_load<QT, ZM, MODE>(b, lane_ok && t < nt, la, rq_a + warp + kWarps * t, q);
     };
-    const bool early = e == 0 && last_red && p.last_red == 1;
+    const bool early = e == 0 && last_red;
     if (early) {  // weights only: legal before the PDL wait
 #pragma unroll
       for (int d = 0; d < PD; ++d) load_quad(buf[d], d);
@@ -429,39 +429,57 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
   }
   if (trace) trace[7] |= (unsigned long long)e << 32;  // segments processed
   if (last_red) {
-    // The S CTAs of row-quad group fj count in; the last one to arrive sums the
-    // group's rows over the S slices in slice order (deterministic, R11); the
-    // others exit at once, freeing their SM for the next kernel.
-    __shared__ unsigned s_last;
+    // Arrival-ordered reduction: the S CTAs of row-quad group fj count in; the
+    // first S - R to arrive exit at once (their SMs go to the next kernel, which
+    // streams its first weights before its own PDL wait), the last R wait for
+    // the group and each sums 1/R of its rows over the S slices in slice order
+    // (deterministic, R11).  R = p.last_red (1 <= R <= S).
+    __shared__ unsigned s_k;
     const int fj = blockIdx.x % J;
+    const int R = min(p.last_red, sh.S);
+    unsigned* arrive = p.counters + fj;
+    unsigned* depart = p.counters + kFusedMaxJ + fj;
     if (e == 0) pdl_wait();  // an empty range never waited: the counters belong to the preceding kernel
     __syncthreads();         // all partial stores of this CTA are issued
     if (tid == 0) {
       __threadfence();
-      const unsigned old = atomicAdd(p.counters + fj, 1u);
-      s_last = old == (unsigned)sh.S - 1;
-      if (s_last) __threadfence();
+      s_k = atomicAdd(arrive, 1u);
     }
     __syncthreads();
-    if (!s_last) return;
+    const int k = (int)s_k;
+    if (k < sh.S - R) return;
+    if (tid == 0) {
+      if (k != sh.S - 1) {
+        while (ld_acquire_u32(arrive) < (unsigned)sh.S) __nanosleep(32);
+      } else {
+        __threadfence();
+      }
+    }
+    __syncthreads();
     if (trace) trace[5] = globaltimer_ns();
-    const int r0 = 4 * (int)((long long)sh.RQ * fj / J);
-    const int r1 = min(sh.m, 4 * (int)((long long)sh.RQ * (fj + 1) / J));
+    const int ri = k - (sh.S - R);
+    const int g0 = (int)((long long)sh.RQ * fj / J), g1 = (int)((long long)sh.RQ * (fj + 1) / J);
+    const int r0 = 4 * (g0 + (int)((long long)(g1 - g0) * ri / R));
+    const int r1 = min(sh.m, 4 * (g0 + (int)((long long)(g1 - g0) * (ri + 1) / R)));
     for (int r = r0 + tid; r < r1; r += kThreads) {
       float v = 0.f;
       const float* pp = p.partial + r;
       for (int ss0 = 0; ss0 < sh.S; ss0 += 16) {
         float t[16];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) t[k] = (ss0 + k < sh.S) ? __ldcg(pp + (size_t)(ss0 + k) * sh.m4) : 0.f;
+        for (int kk = 0; kk < 16; ++kk) t[kk] = (ss0 + kk < sh.S) ? __ldcg(pp + (size_t)(ss0 + kk) * sh.m4) : 0.f;
 #pragma unroll
-        for (int k = 0; k < 16; ++k)
-          if (ss0 + k < sh.S) v += t[k];
+        for (int kk = 0; kk < 16; ++kk)
+          if (ss0 + kk < sh.S) v += t[kk];
       }
       if (p.yf) p.yf[r] = v;
       else p.y[r] = __float2half_rn(v);
     }
-    if (tid == 0) p.counters[fj] = 0u;
+    __syncthreads();
+    if (tid == 0 && atomicAdd(depart, 1u) == (unsigned)R - 1) {  // the last reducer resets the pair
+      *arrive = 0u;
+      *depart = 0u;
+    }
     if (trace) trace[6] = globaltimer_ns();
     return;
   }
@@ -1199,10 +1217,11 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
       // of a group reduces it alone and the others exit early (the next kernel
       // starts streaming on their SMs); large ones keep the parallel group barrier
       const long long red_bytes = (long long)sh.S * 16 * ((sh.RQ + J - 1) / J);
-      p.last_red = red_bytes <= 65536 ? 1 : 0;
-      if (p.xmode == 40) p.last_red = 1;
-      if (p.xmode == 41) p.last_red = 2;
-      if (p.xmode == 42) p.last_red = 0;
+      p.last_red = (int)std::min<long long>(sh.S, (red_bytes + 16383) / 16384);  // ~16 KB of partials per reducer
+      if (p.xmode == 40) p.last_red = 1;       // one reducer per group
+      if (p.xmode == 41) p.last_red = sh.S;    // every CTA of the group reduces (early trigger kept)
+      if (p.xmode == 42) p.last_red = 0;       // group barrier, trigger at the end
+      if (p.xmode >= 43 && p.xmode <= 48) p.last_red = 1 << (p.xmode - 43);  // R = 1, 2, 4, .., 32
     }
   }
   cudaError_t e = sh.compact ? dispatch_q<2>(p, grid, st, batched)
