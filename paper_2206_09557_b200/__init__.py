@@ -20,6 +20,7 @@ from .lutgemm import (  # noqa: F401
     lutgemm_trace_read,
     lutgemm_gemv,
     lutgemm_host_workspace_bytes,
+    lutgemm_launch_count,
     lutgemm_pack_bcq,
     lutgemm_pack_uniform,
     lutgemm_packed_bytes,

@@ -238,6 +238,8 @@ lutgemm_status lutgemm_gemm_host(const lutgemm_weight* w, const uint16_t* X_host
   return LUTGEMM_OK;
 }
 
+uint64_t lutgemm_launch_count(void) { return lg::launch_count(); }
+
 lutgemm_status lutgemm_trace_enable(int on) {
   lg::trace_enable(on);
   return LUTGEMM_OK;

@@ -40,6 +40,8 @@ void trace_enable(int on);
 size_t trace_read(unsigned long long* host, size_t n);
 
 size_t workspace_bytes(const Shape& sh, int b);
+// product kernels (LUT + reduction) this process has launched
+unsigned long long launch_count();
 // padded batch of the batched kernel's partials (1 for the GEMV)
 int batch_pad(int b);
 

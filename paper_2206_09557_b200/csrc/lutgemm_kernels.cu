@@ -35,6 +35,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -209,7 +210,8 @@ __device__ __forceinline__ void ring_load(Ring<QT>& r, bool ok, const LaneAddr& 
 #pragma unroll
     for (int i = 0; i < QT; ++i) {
       if (QT <= 4 || i < q) {
-        r.k[i] = ldg_stream_u4(kp + i * la.kstride);
+        if (MODE == 5) r.k[i] = ldg_stream_u4_256(kp + i * la.kstride);
+        else r.k[i] = ldg_stream_u4(kp + i * la.kstride);
         if (MODE != 4 && (!CMP || i == 0)) r.a[i] = ldg_nc_u2(ap + 8 * i);
         else r.a[i] = make_uint2(0, 0);
       }
@@ -291,7 +293,8 @@ __device__ __forceinline__ float lane_xsum(uint32_t lut, int lane) {
 // ---------------------------------------------------------------------------
 template <int QT, int ZM, int PD, int MODE = 0>
 __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) {
-  constexpr bool HAS_Z = ZM != 0;
+  constexpr bool HAS_Z = ZM != 0, CMP = ZM == 2;
+  constexpr bool RUNPTR = MODE == 7;  // running load pointers, clamped loads, branch-free steady state
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(kFull, tid >> 5, 0);  // warp-uniform for the compiler
@@ -357,8 +360,32 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     // shuffles would otherwise delay it), so PD quads are always in flight
     constexpr int NB = PD + 1;
     Ring<QT> buf[NB];
+    // RUNPTR: the warp's next quad to load is at (lk, lal, lz); each load
+    // advances them by 16 quads unless it was the warp's last quad, so a load
+    // never leaves the warp's range (quads past the end re-read the last one
+    // and are not computed) and needs no predicate or zero-fill
+    const uint8_t* lk = la.kp + (size_t)(rq_a + warp) * la.KB;
+    const uint8_t* lal = la.ap + (size_t)(rq_a + warp) * la.AB;
+    const uint8_t* lz = la.zp + (size_t)(rq_a + warp) * la.ZB;
+    int tl = 0;
     auto load_quad = [&](Ring<QT>& b, int t) {
-      ring_load<QT, ZM, MODE>(b, lane_ok && t < nt, la, rq_a + warp + kWarps * t, q);
+      if constexpr (RUNPTR) {
+#pragma unroll
+        for (int i = 0; i < QT; ++i) {
+          if (QT <= 4 || i < q) {
+            b.k[i] = ldg_stream_u4(lk + i * la.kstride);
+            if (!CMP || i == 0) b.a[i] = ldg_nc_u2(lal + 8 * i);
+          }
+        }
+        if (HAS_Z) b.z = ldg_nc_u2(lz);
+        if (++tl < nt) {
+          lk += (size_t)kWarps * la.KB;
+          lal += (size_t)kWarps * la.AB;
+          if (HAS_Z) lz += (size_t)kWarps * la.ZB;
+        }
+      } else {
+        ring_load<QT, ZM, MODE>(b, lane_ok && t < nt, la, rq_a + warp + kWarps * t, q);
+      }
     };
     const bool early = e == 0 && last_red;
     if (early) {  // weights only: legal before the PDL wait
@@ -399,6 +426,28 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     const float xsum = (HAS_Z && lane_ok) ? lane_xsum(sm.lut, lane) : 0.f;
     float* part = p.partial + (size_t)s * sh.m4;
     // 4. main loop
+    if constexpr (RUNPTR) {
+      float* pw = part + 4 * (rq_a + warp) + (lane >> 3);  // this warp's next partial
+      auto quad = [&](const Ring<QT>& b) {
+        f32x2 acc01, acc23;
+        ring_compute<QT, ZM, 0>(b, lc, xsum, acc01, acc23, q, false);
+        if (!lane_ok) acc01 = acc23 = 0ull;  // tail-slice lanes loaded lane 0's words
+        const float v = reduce4(acc01, acc23, lane);
+        if ((lane & 7) == 0) *pw = v;
+        pw += 4 * kWarps;
+      };
+      int t0 = 0;
+      for (; t0 + NB <= nt; t0 += NB) {
+#pragma unroll
+        for (int d = 0; d < NB; ++d) {
+          load_quad(buf[(d + PD) % NB], 0);
+          quad(buf[d]);
+        }
+      }
+#pragma unroll
+      for (int d = 0; d < NB - 1; ++d)
+        if (t0 + d < nt) quad(buf[d]);
+    } else
     for (int t0 = 0; t0 < nt; t0 += NB) {
       if (tid == 0 && pf_steps > 0) {  // optional L2 prefetch pf_steps steps ahead of warp 0
         const int lo = rq_a + kWarps * (t0 + pf_steps);
@@ -995,8 +1044,11 @@ static cudaLaunchAttribute g_pdl_attr = [] {
   return a;
 }();
 
+std::atomic<unsigned long long> g_launches{0};  // product kernels launched by this process (lutgemm_launch_count)
+
 template <typename K>
 static cudaError_t launch(K kernel, int grid, const KParams& p, cudaStream_t st, int threads = kThreads) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
   if (err != cudaSuccess) return err;
   cudaLaunchConfig_t cfg = {};
@@ -1010,6 +1062,7 @@ static cudaError_t launch(K kernel, int grid, const KParams& p, cudaStream_t st,
 }
 
 static cudaError_t launch_reduce(const KParams& p, cudaStream_t st) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   static bool attr_set = false;
   if (!attr_set) {  // keep the max-shared-memory carveout: no L1/smem reconfiguration between the two kernels
     cudaFuncSetAttribute(lut_reduce_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -1041,11 +1094,16 @@ static cudaError_t launch_gemv_t(const KParams& p, int grid, cudaStream_t st) {
       case 16: return launch(lut_gemv_kernel<QT, ZM, 2, 4>, grid, p, st);
       case 14: return launch(lut_gemv_kernel<QT, ZM, 3, 0>, grid, p, st);
       case 18: return launch(lut_gemv_kernel<QT, ZM, 4, 0>, grid, p, st);
+      case 15: return launch(lut_gemv_kernel<QT, ZM, 2, 5>, grid, p, st);
+      case 19: return launch(lut_gemv_kernel<QT, ZM, 3, 5>, grid, p, st);
+      case 20: return launch(lut_gemv_kernel<QT, ZM, 2, 7>, grid, p, st);
+      case 21: return launch(lut_gemv_kernel<QT, ZM, 3, 7>, grid, p, st);
       default: break;
     }
     }
   }
-  return launch(lut_gemv_kernel<QT, ZM, PD>, grid, p, st);
+  if (p.xmode == 22) return launch(lut_gemv_kernel<QT, ZM, PD, 0>, grid, p, st);  // predicated per-quad loads (old)
+  return launch(lut_gemv_kernel<QT, ZM, PD, 7>, grid, p, st);
 }
 
 // batched: V-wide slots (V = 2 only for b = 2); p.qpw = row quads per work item
@@ -1070,6 +1128,7 @@ static cudaError_t launch_batched_t(const KParams& p, int grid, cudaStream_t st)
 }
 
 static cudaError_t launch_reduce_batched(const KParams& p, cudaStream_t st) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((p.sh.m4 + 63) / 64);
   cfg.blockDim = dim3(256);
@@ -1137,6 +1196,8 @@ static int g_pf_steps = -1;
 static unsigned long long* g_trace = nullptr;
 static bool g_trace_on = false;
 constexpr int kTraceMaxCtas = 1024;
+
+unsigned long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 void trace_enable(int on) {
   g_trace_on = on != 0;

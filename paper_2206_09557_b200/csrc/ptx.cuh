@@ -85,6 +85,14 @@ __device__ __forceinline__ uint4 ldg_stream_u4(const void* p) {
   return r;
 }
 
+// as ldg_stream_u4 with the L2 256-byte sector-promotion hint (regions are 256-byte aligned)
+__device__ __forceinline__ uint4 ldg_stream_u4_256(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
 __device__ __forceinline__ uint2 ldg_nc_u2(const void* p) {
   uint2 r;
   asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));

@@ -61,6 +61,7 @@ SIGNATURES = [
     ("lutgemm_gemm_host", _I, [ctypes.POINTER(lutgemm_weight), _P, _I, _P, _P, _SZ, _P]),
     ("lutgemm_trace_enable", _I, [_I]),
     ("lutgemm_trace_read", _SZ, [ctypes.POINTER(ctypes.c_uint64), _SZ]),
+    ("lutgemm_launch_count", ctypes.c_uint64, []),
     ("lutgemm_tp_unique_id", _I, [_P]),
     ("lutgemm_tp_init", _I, [_I, _I, _P, ctypes.POINTER(_P)]),
     ("lutgemm_tp_workspace_bytes", _SZ, [_P, _I, _I, _I, _I]),
@@ -272,3 +273,8 @@ class TPComm:
         if self.handle:
             _check("lutgemm_tp_destroy", lib.lutgemm_tp_destroy(self.handle))
             self.handle = None
+
+
+def lutgemm_launch_count() -> int:
+    """Product kernels launched by this process through the library (host-side count)."""
+    return int(lib.lutgemm_launch_count())
