@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
       auto quad = [&](const Ring<QT>& b) {
         f32x2 acc01, acc23;
         ring_compute<QT, ZM, 0>(b, lc, xsum, acc01, acc23, q, false);
-        if (!lane_ok) acc01 = acc23 = 0ull;  // tail-slice lanes loaded lane 0's words
+        if (Ls < kLanesPerSlice && !lane_ok) acc01 = acc23 = 0ull;  // tail-slice lanes loaded lane 0's words
         const float v = reduce4(acc01, acc23, lane);
         if ((lane & 7) == 0) *pw = v;
         pw += 4 * kWarps;
@@ -491,8 +491,14 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     if (e == 0) pdl_wait();  // an empty range never waited: the counters belong to the preceding kernel
     __syncthreads();         // all partial stores of this CTA are issued
     if (tid == 0) {
-      __threadfence();
-      s_k = atomicAdd(arrive, 1u);
+      // release: the CTA's partial stores (ordered before by the barrier) are
+      // visible to whoever acquires the count; acquire: the last arriver sees all
+      if (p.xmode == 23) {
+        __threadfence();
+        s_k = atomicAdd(arrive, 1u);
+      } else {
+        s_k = atom_add_acq_rel_u32(arrive, 1u);
+      }
     }
     __syncthreads();
     const int k = (int)s_k;
@@ -500,7 +506,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     if (tid == 0) {
       if (k != sh.S - 1) {
         while (ld_acquire_u32(arrive) < (unsigned)sh.S) __nanosleep(32);
-      } else {
+      } else if (p.xmode == 23) {
         __threadfence();
       }
     }
