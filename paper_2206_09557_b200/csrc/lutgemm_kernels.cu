@@ -370,6 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     int tl = 0;
     auto load_quad = [&](Ring<QT>& b, int t) {
       if constexpr (RUNPTR) {
+        if (nt == 0) return;  // a warp without quads in the segment loads nothing (its first quad is past the range)
 #pragma unroll
         for (int i = 0; i < QT; ++i) {
           if (QT <= 4 || i < q) {
