@@ -1,0 +1,26 @@
+"""compute-sanitizer over every kernel path (tier T4): memcheck and
+racecheck on tools/sanitize_case.py (GEMV fused/non-fused, tails, batched V=2
+and V=4, compact format; each result also checked against the oracle)."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
+def test_sanitizer_clean(tool):
+    if not os.path.exists(SAN):
+        pytest.skip("compute-sanitizer not installed")
+    r = subprocess.run([SAN, "--tool", tool, "--error-exitcode", "9", "--print-limit", "10", sys.executable,
+                        os.path.join(ROOT, "tools", "sanitize_case.py")], capture_output=True, text=True, timeout=900,
+                       cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "sanitize cases done" in out
+    assert ("0 errors" in out) or ("0 hazards" in out), out[-2000:]
