@@ -139,6 +139,32 @@ lutgemm_status lutgemm_pack_bcq(const lutgemm_pack_src* src, lutgemm_weight* dst
 lutgemm_status lutgemm_unpack_bcq(const lutgemm_weight* w, uint32_t* planes, uint16_t* alpha,
                                   uint16_t* offset, void* stream);
 
+/* ---- Quantizers (the offline step before the path) ----
+ * Input: a dense weight W, device fp16 [m][n] row-major; same shape rules as
+ * every call (n % 32 == 0, g as above).  Outputs are the canonical pack
+ * sources above (device buffers, caller-owned), so a dense layer becomes a
+ * packed weight with quantize_* followed by lutgemm_pack_bcq.  Offline,
+ * asynchronous on `stream`, deterministic.
+ *
+ * RTN (the "RTN" baseline of Tables 3/6; conventions of SPEC S:L112-120): per
+ * (row, group) s = fp16((max - min)/(2^q - 1)), z_hat = fp16(min) and
+ * code = clamp(rint((w - z_hat)/s), 0, 2^q - 1) from the stored s and z_hat; a
+ * constant group stores s = 1, codes 0.  Writes codes uint8 [m][n], scale and
+ * zero fp16 [m][n/g] -- a LUTGEMM_SRC_UNIFORM(_COMPACT) source (App. C). */
+lutgemm_status lutgemm_quantize_rtn(const uint16_t* W, int m, int n, int q, int g, uint8_t* codes, uint16_t* scale,
+                                    uint16_t* zero, void* stream);
+
+/* BCQ (Sec. 2.3; the "iterative solver" of App. E): greedy
+ * residual fit per (row, group) -- b_i = sign(r) (sign(0) = +1), alpha_i =
+ * fp16(mean |r|), r -= alpha_i b_i -- then `iters` alternating rounds (0 =
+ * greedy only): alpha = least squares for the fixed signs (fp64 solve; a
+ * singular B^T B keeps the previous alpha), then every element's signs = the
+ * nearest of the 2^q levels sum_i +-alpha_i.  Writes planes uint32
+ * [q][m][n/32] and alpha fp16 [m][n/g][q] -- a LUTGEMM_SRC_BCQ source.
+ * LUTGEMM_ERR_INVALID_ARG if q * g / 8 + 2^(q+2) bytes exceed shared memory. */
+lutgemm_status lutgemm_quantize_bcq(const uint16_t* W, int m, int n, int q, int g, int iters, uint32_t* planes,
+                                    uint16_t* alpha, void* stream);
+
 /* Workspace for a product with m rows, n columns, batch b: fp32 split-K
  * partials plus row-block arrival counters.  The workspace must be zeroed
  * once (lutgemm_workspace_init) before its first use; every successful call
@@ -185,6 +211,12 @@ lutgemm_status lutgemm_gemm_host(const lutgemm_weight* w, const uint16_t* X_host
  * n values to host memory (synchronous) and returns how many it copied. */
 lutgemm_status lutgemm_trace_enable(int on);
 size_t lutgemm_trace_read(uint64_t* host, size_t n);
+
+/* Number of product kernels (LUT-GEMV / LUT-GEMM and their reduction
+ * kernels, not pack kernels) this process has launched through the library --
+ * host-side count; a CUDA graph replay re-runs the launches captured in it
+ * without counting them again.  For benchmark accounting. */
+uint64_t lutgemm_launch_count(void);
 
 /* ---------------- Tensor parallelism over NCCL (NVLink / NVSwitch) ----------------
  * The paper runs LUT-GEMM tensor-parallel on 1/2/4/8 GPUs (P:L378-385,

@@ -23,6 +23,8 @@ from .lutgemm import (  # noqa: F401
     lutgemm_launch_count,
     lutgemm_pack_bcq,
     lutgemm_pack_uniform,
+    lutgemm_quantize_bcq,
+    lutgemm_quantize_rtn,
     lutgemm_packed_bytes,
     lutgemm_unpack_bcq,
     lutgemm_workspace_bytes,

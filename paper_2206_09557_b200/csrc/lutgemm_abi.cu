@@ -240,6 +240,37 @@ lutgemm_status lutgemm_gemm_host(const lutgemm_weight* w, const uint16_t* X_host
 
 uint64_t lutgemm_launch_count(void) { return lg::launch_count(); }
 
+lutgemm_status lutgemm_quantize_rtn(const uint16_t* W, int m, int n, int q, int g, uint8_t* codes, uint16_t* scale,
+                                    uint16_t* zero, void* stream) {
+  lutgemm_status st = check_shape(m, n, q, g);
+  if (st != LUTGEMM_OK) return st;
+  if (!W || !codes || !scale || !zero) return fail(LUTGEMM_ERR_INVALID_ARG, "W, codes, scale and zero must be non-NULL");
+  if (!aligned(W, 2) || !aligned(scale, 2) || !aligned(zero, 2))
+    return fail(LUTGEMM_ERR_MISALIGNED, "fp16 buffers must be 2-byte aligned");
+  st = check_device();
+  if (st != LUTGEMM_OK) return st;
+  cudaError_t e = lg::run_quantize_rtn(W, m, n, q, g, codes, scale, zero, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "quantize_rtn kernel launch");
+  return LUTGEMM_OK;
+}
+
+lutgemm_status lutgemm_quantize_bcq(const uint16_t* W, int m, int n, int q, int g, int iters, uint32_t* planes,
+                                    uint16_t* alpha, void* stream) {
+  lutgemm_status st = check_shape(m, n, q, g);
+  if (st != LUTGEMM_OK) return st;
+  if (iters < 0 || iters > 1000) return fail(LUTGEMM_ERR_INVALID_ARG, "iters=%d must be in [0, 1000]", iters);
+  if (!W || !planes || !alpha) return fail(LUTGEMM_ERR_INVALID_ARG, "W, planes and alpha must be non-NULL");
+  if (!aligned(W, 2) || !aligned(planes, 4) || !aligned(alpha, 2))
+    return fail(LUTGEMM_ERR_MISALIGNED, "buffers must be element-aligned");
+  if (lg::quantize_bcq_smem_per_warp(q, g) > 227u * 1024u)
+    return fail(LUTGEMM_ERR_INVALID_ARG, "group of %d columns with q=%d exceeds the per-warp shared memory", g, q);
+  st = check_device();
+  if (st != LUTGEMM_OK) return st;
+  cudaError_t e = lg::run_quantize_bcq(W, m, n, q, g, iters, planes, alpha, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "quantize_bcq kernel launch");
+  return LUTGEMM_OK;
+}
+
 lutgemm_status lutgemm_trace_enable(int on) {
   lg::trace_enable(on);
   return LUTGEMM_OK;

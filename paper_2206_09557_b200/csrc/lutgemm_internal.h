@@ -58,6 +58,13 @@ cudaError_t run_pack_uniform(const Shape& sh, const uint8_t* codes, const uint16
 cudaError_t run_unpack(const Shape& sh, const void* src, uint32_t* planes, uint16_t* alpha, uint16_t* offset,
                        cudaStream_t st);
 
+// quantizers: dense fp16 W [m][n] -> canonical pack sources
+cudaError_t run_quantize_rtn(const uint16_t* W, int m, int n, int q, int g, uint8_t* codes, uint16_t* scale,
+                             uint16_t* zero, cudaStream_t st);
+cudaError_t run_quantize_bcq(const uint16_t* W, int m, int n, int q, int g, int iters, uint32_t* planes,
+                             uint16_t* alpha, cudaStream_t st);
+size_t quantize_bcq_smem_per_warp(int q, int g);
+
 // TP helpers
 cudaError_t run_cast_f32_f16(const float* src, uint16_t* dst, size_t count, cudaStream_t st);
 // src [P][b][ms] -> dst [b][P*ms]

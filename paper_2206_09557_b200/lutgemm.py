@@ -62,6 +62,8 @@ SIGNATURES = [
     ("lutgemm_trace_enable", _I, [_I]),
     ("lutgemm_trace_read", _SZ, [ctypes.POINTER(ctypes.c_uint64), _SZ]),
     ("lutgemm_launch_count", ctypes.c_uint64, []),
+    ("lutgemm_quantize_rtn", _I, [_P, _I, _I, _I, _I, _P, _P, _P, _P]),
+    ("lutgemm_quantize_bcq", _I, [_P, _I, _I, _I, _I, _I, _P, _P, _P]),
     ("lutgemm_tp_unique_id", _I, [_P]),
     ("lutgemm_tp_init", _I, [_I, _I, _P, ctypes.POINTER(_P)]),
     ("lutgemm_tp_workspace_bytes", _SZ, [_P, _I, _I, _I, _I]),
@@ -278,3 +280,29 @@ class TPComm:
 def lutgemm_launch_count() -> int:
     """Product kernels launched by this process through the library (host-side count)."""
     return int(lib.lutgemm_launch_count())
+
+
+def lutgemm_quantize_rtn(W: torch.Tensor, q: int, g: int, stream=None):
+    """Dense fp16 W [m][n] (CUDA) -> (codes uint8 [m][n], scale fp16 [m][n/g], zero fp16 [m][n/g]): RTN."""
+    if W.dtype != torch.float16 or not W.is_cuda or not W.is_contiguous():
+        raise ValueError("W must be a contiguous CUDA fp16 tensor")
+    m, n = int(W.shape[0]), int(W.shape[1])
+    codes = torch.empty((m, n), dtype=torch.uint8, device=W.device)
+    scale = torch.empty((m, n // g), dtype=torch.float16, device=W.device)
+    zero = torch.empty((m, n // g), dtype=torch.float16, device=W.device)
+    _check("lutgemm_quantize_rtn", lib.lutgemm_quantize_rtn(W.data_ptr(), m, n, q, g, codes.data_ptr(),
+                                                            scale.data_ptr(), zero.data_ptr(), _stream(stream)))
+    return codes, scale, zero
+
+
+def lutgemm_quantize_bcq(W: torch.Tensor, q: int, g: int, iters: int = 0, stream=None):
+    """Dense fp16 W [m][n] (CUDA) -> (planes int32 [q][m][n/32], alpha fp16 [m][n/g][q]): greedy BCQ
+    plus `iters` alternating rounds."""
+    if W.dtype != torch.float16 or not W.is_cuda or not W.is_contiguous():
+        raise ValueError("W must be a contiguous CUDA fp16 tensor")
+    m, n = int(W.shape[0]), int(W.shape[1])
+    planes = torch.empty((q, m, n // 32), dtype=torch.int32, device=W.device)
+    alpha = torch.empty((m, n // g, q), dtype=torch.float16, device=W.device)
+    _check("lutgemm_quantize_bcq", lib.lutgemm_quantize_bcq(W.data_ptr(), m, n, q, g, iters, planes.data_ptr(),
+                                                            alpha.data_ptr(), _stream(stream)))
+    return planes, alpha

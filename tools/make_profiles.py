@@ -142,7 +142,10 @@ def main(tag, rnd="01"):
     open(os.path.join(PROF, f"r{rnd}_ncu_fc1.md"), "w").write("\n".join(lines) + "\n")
 
     # sweep table
-    sw = [json.loads(l) for l in open(p(f"sweep_{tag}.jsonl")) if l.strip().startswith("{")]
+    allsw = [json.loads(l) for l in open(p(f"sweep_{tag}.jsonl")) if l.strip().startswith("{")]
+    sw = [d for d in allsw if not d["case"].startswith(("dense", "quantize"))]
+    quant = [d for d in allsw if d["case"].startswith("quantize")]
+    dense = {d["b"]: d for d in allsw if d["case"].startswith("dense")}
     t = [f"# Round {int(rnd)} -- all BASELINE shapes (tools/sweep.py, CUDA-graph timing, B200), tag {tag}", "",
          "Timing: CUDA graph of consecutive products on rotating weight copies (> 3x L2), events around the replays;"
          " us per product. Peak = measured 6544.7 GB/s (`MEASURED_PEAKS.json`). LDS roof = fp32 LUT bytes /"
@@ -154,11 +157,21 @@ def main(tag, rnd="01"):
             t.append(f"| {d['case']} | {d['m']} | {d['n']} | {d['q']} | {d['g']} | {d['offset']} | "
                      f"{d.get('compact', False)} | {d['us']} | {d['GBps']} | {100 * d['frac_hbm']:.1f} | {d['hbm_roof_us']} |")
     t += ["", "## batched fc1 (b = 2..32): the shared-memory lookup roof binds from b = 2 (P:L529-530)", "",
-          "| b | us | HBM roof us | LDS roof us | % of binding roof |", "|---|---|---|---|---|"]
-    for d in sw:
-        if d["b"] > 1:
-            t.append(f"| {d['b']} | {d['us']} | {d['hbm_roof_us']} | {d['lds_roof_us']} | "
-                     f"{100 * d['frac_of_binding_roof']:.1f} |")
+          "| b | us | HBM roof us | LDS roof us | % of binding roof | context: dense fp16 cuBLAS us |",
+          "|---|---|---|---|---|---|"]
+    for d in [x for x in sw if x["b"] == 1 and x["case"] == "fc1"] + [x for x in sw if x["b"] > 1]:
+        dn = dense.get(d["b"], {}).get("us", "")
+        t.append(f"| {d['b']} | {d['us']} | {d['hbm_roof_us']} | {d['lds_roof_us']} | "
+                 f"{100 * d['frac_of_binding_roof']:.1f} | {dn} |")
+    if dense:
+        t += ["", "Dense fp16 (cuBLAS through torch.matmul, 1.21 GB weight, rotating copies) is a comparison system, "
+              "context only (SURVEY K2): it shows where the LUT method's shared-memory roof (P:L529-530) makes a "
+              "dense fp16 product faster."]
+    if quant:
+        t += ["", "## Quantizers (offline step before the path, NEXT-4): dense fp16 fc1 49152 x 12288 -> pack sources", "",
+              "| quantizer | q | g | ms | fp16 input GB/s |", "|---|---|---|---|---|"]
+        for d in quant:
+            t.append(f"| {d['case'][9:]} | {d['q']} | {d['g']} | {d['ms']} | {d['GBps_fp16_in']} |")
     t += ["", "## 96-layer OPT-175B decoder linear stack (tools/stack.py), one token, 1 GPU", "",
           f"{stack['ms_per_token']} ms per token ({stack['GBps_per_gpu']} GB/s over "
           f"{stack['weight_bytes_per_gpu'] / 1e9:.1f} GB of packed weights); per linear (eager): "

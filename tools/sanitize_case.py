@@ -44,6 +44,19 @@ def main():
         y = (L.lutgemm_gemv(w, dev(X)[0])[None] if b == 1 else L.lutgemm_gemm_batched(w, dev(X))).float().cpu().numpy()
         planes, alpha, z = O.uniform_to_bcq(u["codes"], u["scale"], u["zero"], q)
         check(y.astype(np.float64), O.bcq_gemv(planes, O.store_fp16(alpha), O.store_fp16(z), X, n, g), ("compact", b))
+    # quantizers (NEXT-4): RTN and greedy / alternating BCQ, bit-exact vs the oracle
+    import oracle.quantize_oracle as Q
+    rng = np.random.default_rng(3)
+    W = (rng.standard_normal((9, 1024)) * 0.05).astype(np.float16)
+    c, sc, z = L.lutgemm_quantize_rtn(dev(W), 3, 128)
+    rc, rs, rz = Q.quantize_rtn(W, 3, 128)
+    assert np.array_equal(c.cpu().numpy(), rc) and np.array_equal(sc.cpu().numpy(), rs)
+    print("ok quantize_rtn", flush=True)
+    for iters in (0, 2):
+        p, a = L.lutgemm_quantize_bcq(dev(W), 3, 128, iters)
+        rp, ra = Q.quantize_bcq_greedy(W, 3, 128) if iters == 0 else Q.quantize_bcq_alternating(W, 3, 128, iters)
+        assert np.array_equal(p.cpu().numpy().view(np.uint32), rp) and np.array_equal(a.cpu().numpy(), ra)
+        print(f"ok quantize_bcq iters={iters}", flush=True)
     torch.cuda.synchronize()
     print("sanitize cases done")
 

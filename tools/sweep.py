@@ -97,9 +97,65 @@ def case(name, m, n, q, g, b=1, uniform=False, steps=400, seed=7, compact=False)
     return out
 
 
+def dense_fp16(m, n, b, steps=200):
+    """Context only (a comparison system): cuBLAS fp16 Y = X W^T on a
+    dense fp16 weight of the same shape, rotating copies > 3x L2, graph-timed."""
+    dev = torch.device("cuda")
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    nc = max(2, math.ceil(3 * l2 / (2 * m * n)))
+    Ws = [torch.randn(m, n, device=dev, dtype=torch.float16) * 0.01 for _ in range(nc)]
+    X = torch.randn(b, n, device=dev, dtype=torch.float16)
+    Y = torch.empty(b, m, device=dev, dtype=torch.float16)
+    for i in range(3):
+        torch.matmul(X, Ws[i % nc].t(), out=Y)
+    torch.cuda.synchronize()
+    G = nc * max(1, 20 // nc)
+    g = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream()
+    cap.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.graph(g, stream=cap):
+        for i in range(G):
+            torch.matmul(X, Ws[i % nc].t(), out=Y)
+    g.replay()
+    torch.cuda.synchronize()
+    reps = max(1, steps // G)
+    a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        g.replay()
+    e.record()
+    torch.cuda.synchronize()
+    us = a.elapsed_time(e) / (reps * G) * 1e3
+    print(json.dumps({"case": f"dense_fp16_cublas_fc1_b{b}", "m": m, "n": n, "b": b, "us": round(us, 3),
+                      "bytes": 2 * m * n, "GBps": round(2 * m * n / (us * 1e-6) / 1e9, 1),
+                      "note": "context only: dense fp16 weight (4.7x the packed q=3 bytes), cuBLAS via torch.matmul"}),
+          flush=True)
+    del Ws
+    torch.cuda.empty_cache()
+
+
+def quantizers(m, n, q, g):
+    """Offline step (NEXT-4): time the GPU quantizers on a dense fp16 layer (eager, events)."""
+    dev = torch.device("cuda")
+    W = (torch.randn(m, n, device=dev) * 0.02).to(torch.float16)
+    for name, fn in (("rtn", lambda: L.lutgemm_quantize_rtn(W, q, g)),
+                     ("bcq_greedy", lambda: L.lutgemm_quantize_bcq(W, q, g, 0)),
+                     ("bcq_alternating_3", lambda: L.lutgemm_quantize_bcq(W, q, g, 3))):
+        fn()
+        torch.cuda.synchronize()
+        a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        e.record()
+        torch.cuda.synchronize()
+        print(json.dumps({"case": f"quantize_{name}", "m": m, "n": n, "q": q, "g": g, "b": 0,
+                          "ms": round(a.elapsed_time(e), 3),
+                          "GBps_fp16_in": round(2 * m * n / (a.elapsed_time(e) * 1e-3) / 1e9, 1)}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="attn,ffn,llama,batched")
+    ap.add_argument("--only", default="attn,ffn,llama,batched,dense,quant")
     ap.add_argument("--cases", default="", help="comma list of m:n:q:g[:b[:u]] instead of --only")
     ap.add_argument("--steps", type=int, default=400)
     args = ap.parse_args()
@@ -130,6 +186,11 @@ def main():
     if "batched" in only:
         for b in (2, 4, 8, 16, 32):
             case(f"fc1_b{b}", 49152, 12288, 3, 128, b=b, steps=max(20, args.steps // (4 * b)))
+    if "quant" in only:
+        quantizers(49152, 12288, 3, 128)
+    if "dense" in only:
+        for b in (1, 2, 4, 8, 16, 32):
+            dense_fp16(49152, 12288, b)
 
 
 if __name__ == "__main__":
