@@ -177,6 +177,22 @@ def main(tag, rnd="01"):
           f"{stack['weight_bytes_per_gpu'] / 1e9:.1f} GB of packed weights); per linear (eager): "
           f"{stack['per_linear_us_eager']}.", f"Paper context: {stack['paper_context_ms']}.", ""]
     open(os.path.join(PROF, f"r{rnd}_sweep.md"), "w").write("\n".join(t) + "\n")
+    # sanitizers (tools/sanitize.sh), if that run is present
+    san = {t: os.path.join(OUT, f"sanitize_{t}.txt") for t in ("memcheck", "racecheck", "synccheck", "initcheck")}
+    if all(os.path.exists(v) for v in san.values()):
+        sl = [f"# Round {int(rnd)} -- compute-sanitizer over every kernel path (SURVEY 4, tier T4)", "",
+              "Command: `bash tools/sanitize.sh` (runs `tools/sanitize_case.py` under each tool: GEMV fused and "
+              "non-fused with one and many reducers, n and m tails, batched V=2 and V=4, q up to 6, fp32 output, "
+              "compact uniform format, the RTN / greedy / alternating quantizers; every result is checked against "
+              "the oracle).", "", "| tool | result | oracle checks passed |", "|---|---|---|"]
+        for t, f in san.items():
+            txt = open(f).read()
+            summ = [l.replace("========= ", "") for l in txt.splitlines() if "SUMMARY" in l]
+            sl.append(f"| {t} | {summ[-1] if summ else '?'} | {txt.count(chr(10) + 'ok ') + txt.startswith('ok ')} |")
+        sl += ["", "History: the first initcheck run found reads of uninitialised bytes -- warps without any row quad "
+               "in a non-fused segment still issued their clamped ring loads at a quad past the range. Fixed (such "
+               "warps load nothing); all four tools are clean since."]
+        open(os.path.join(PROF, f"r{rnd}_sanitizers.md"), "w").write("\n".join(sl) + "\n")
     print("profiles written for", tag)
 
 
