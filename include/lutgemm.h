@@ -27,7 +27,7 @@
  *    thread-local error text; calls on distinct outputs/workspaces are
  *    thread-safe.
  *  - Supported shapes on the GPU path: n % 32 == 0, n % g == 0 and
- *    g in {32, 64, 128, 256, 512, 1024} or g a multiple of 1024 or g == n
+ *    g in {32, 64, 128, 256, 512, 1024} or g a multiple of 1024 or g == n (any n)
  *    (g == n is row-wise, P:L496 '-' / P:L392 "g=m"); 1 <= q <= 8, m >= 1,
  *    1 <= b <= 32.  Anything else returns LUTGEMM_ERR_INVALID_ARG (DESIGN.md
  *    reading R13: the paper does not define chunks straddling a group; the

@@ -32,7 +32,8 @@ lutgemm_status check_shape(int m, int n, int q, int g) {
   if (m < 1) return fail(LUTGEMM_ERR_INVALID_ARG, "m=%d must be >= 1", m);
   if (n < 32 || n % 32) return fail(LUTGEMM_ERR_INVALID_ARG, "n=%d must be a positive multiple of 32", n);
   if (q < 1 || q > 8) return fail(LUTGEMM_ERR_INVALID_ARG, "q=%d must be in [1, 8]", q);
-  const bool g_ok = (g >= 32 && g <= 1024 && (1024 % g) == 0) || (g > 1024 && (g % 1024 == 0 || g == n));
+  // a power of two up to one LUT slice, whole slices, or row-wise (g == n, any multiple of 32)
+  const bool g_ok = (g >= 32 && g <= 1024 && (1024 % g) == 0) || (g > 1024 && g % 1024 == 0) || g == n;
   if (!g_ok || n % g)
     return fail(LUTGEMM_ERR_INVALID_ARG,
                 "g=%d must divide n=%d and be one of 32..1024 (power of two), a multiple of 1024, or n", g, n);

@@ -281,3 +281,43 @@ def test_gemv_reduction_modes(monkeypatch, xmode, m, n, q, g, off):
     assert np.array_equal(run(w, X, f32=True), y)
     monkeypatch.delenv("LUTGEMM_XMODE")
     assert_parity(y, O.bcq_gemv(d["planes"], d["alpha"], d["offset"], X, n, g), (m, n, q, g, xmode))
+
+
+def _random_configs(k=24, seed=2206):
+    """Seeded random shapes over the whole supported space: m and n tails, q 1..8, every g kind
+    (32..1024 powers of two, multiples of 1024, row-wise), b 1..32, offset / compact uniform."""
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < k:
+        q = int(rng.integers(1, 9))
+        n = 32 * int(rng.integers(1, 200))
+        kind = rng.integers(0, 3)
+        if kind == 0:
+            g = int(2 ** rng.integers(5, 11))
+        elif kind == 1:
+            g = 1024 * int(rng.integers(1, 4))
+        else:
+            g = n
+        if n % g:
+            continue
+        m = int(rng.integers(1, 3000))
+        b = int(rng.choice([1, 1, 2, 3, 4, 8, 13, 32]))
+        fmt = int(rng.integers(0, 3))  # 0 BCQ, 1 BCQ + offset, 2 uniform compact
+        out.append((m, n, q, g, b, fmt))
+    return out
+
+
+@pytest.mark.parametrize("m,n,q,g,b,fmt", _random_configs())
+def test_random_shapes_full_parity(m, n, q, g, b, fmt):
+    import paper_2206_09557_b200 as L
+    X = gen_x(m + b, b, n)
+    if fmt == 2:
+        u = gen_uniform(m + n + q, m, n, q, g)
+        w = L.lutgemm_pack_uniform(dev(u["codes"]), dev(u["scale"]), dev(u["zero"]), q, g, compact=True)
+        planes, alpha, z = O.uniform_to_bcq(u["codes"], u["scale"], u["zero"], q)
+        ref = O.bcq_gemv(planes, O.store_fp16(alpha), O.store_fp16(z), X, n, g)
+    else:
+        d = gen_bcq(m + n + q, m, n, q, g, offset=fmt == 1)
+        w = pack(d)
+        ref = O.bcq_gemv(d["planes"], d["alpha"], d["offset"], X, n, g)
+    assert_parity(run(w, X), ref, (m, n, q, g, b, fmt))
