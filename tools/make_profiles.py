@@ -150,12 +150,22 @@ def main(tag, rnd="01"):
          "Timing: CUDA graph of consecutive products on rotating weight copies (> 3x L2), events around the replays;"
          " us per product. Peak = measured 6544.7 GB/s (`MEASURED_PEAKS.json`). LDS roof = fp32 LUT bytes /"
          " (128 B/clk/SM x 148 SMs x 1.965 GHz).", "", "## b = 1 (GEMV)", "",
-         "| case | m | n | q | g | offset | compact | us | GB/s | % of HBM peak | HBM roof us |",
-         "|---|---|---|---|---|---|---|---|---|---|---|"]
+         "| case | m | n | q | g | offset | compact | compression vs fp16 | us | GB/s | % of HBM peak | HBM roof us |",
+         "|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for d in sw:
         if d["b"] == 1:
+            cr = 2 * d["m"] * d["n"] / (d["bytes_alg"] - 2 * d["n"] - 2 * d["m"])
             t.append(f"| {d['case']} | {d['m']} | {d['n']} | {d['q']} | {d['g']} | {d['offset']} | "
-                     f"{d.get('compact', False)} | {d['us']} | {d['GBps']} | {100 * d['frac_hbm']:.1f} | {d['hbm_roof_us']} |")
+                     f"{d.get('compact', False)} | {cr:.2f}x | {d['us']} | {d['GBps']} | {100 * d['frac_hbm']:.1f} | "
+                     f"{d['hbm_roof_us']} |")
+    att = sorted([d for d in sw if d["case"].startswith("attn_")], key=lambda d: d["bytes_alg"])
+    if att:
+        t += ["", "Latency vs compression ratio on the 12288 x 12288 layer (the analogue of Fig. 4(b), P:L309-313: "
+              "for batch 1 the latency follows the memory footprint; (q, g) pairs of similar footprint take "
+              "similar time):", "", "| q | g | compression vs fp16 | MB | us |", "|---|---|---|---|---|"]
+        for d in att:
+            t.append(f"| {d['q']} | {d['g']} | {2 * d['m'] * d['n'] / d['bytes_alg']:.2f}x | "
+                     f"{d['bytes_alg'] / 1e6:.1f} | {d['us']} |")
     t += ["", "## batched fc1 (b = 2..32): the shared-memory lookup roof binds from b = 2 (P:L529-530)", "",
           "| b | us | HBM roof us | LDS roof us | % of binding roof | context: dense fp16 cuBLAS us |",
           "|---|---|---|---|---|---|"]
