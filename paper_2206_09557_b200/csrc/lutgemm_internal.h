@@ -24,12 +24,8 @@ struct KParams {
   int spi;           // batched: LUT slices per work item (split-K factor S2 = ceil(S / spi))
   int qpw;           // batched: row quads per work item (256 or 128)
   int gsh;           // batched: layout lane -> slice-local group shift (31: one group per slice)
-  int pf_steps;      // GEMV: L2 prefetch distance in 16-quad steps
-  int pf_init;       // GEMV: 16-quad steps bulk-prefetched into L2 before the PDL wait
-  int xmode;         // experiment knob (0 default)
   int fused_J;       // GEMV: CTAs per slice in the fused-reduction mode (0: separate reduction kernel)
-  int last_red;      // GEMV fused mode: R > 0 = the last R CTAs to arrive in a row-quad group reduce it, the others
-                     //   exit early (early PDL trigger, weights streamed before the PDL wait); 0 = group barrier
+  int reducers;      // GEMV fused mode: the last R CTAs to arrive in a row-quad group reduce it
   long long items;
   unsigned long long* trace;  // optional per-CTA timeline (kTraceSlots u64 per CTA), or null
 };

@@ -9,28 +9,27 @@
 // slices -- here in a fixed order instead of atomicAdd (R11).
 //
 // B200 design:
-//  * one persistent CTA per SM (512 threads, 16 warps), a balanced static
-//    split of (slice, row-quad) work items;
-//  * mu = 8, fp32 LUT entries, 128 tables x 256 entries = 128 KB of shared
-//    memory per 1024-column slice, stored interleaved so that entry k of the
-//    table used by lane l at chunk step j lives at
+//  * GEMV: one CTA per SM (512 threads, 16 warps), J CTAs per 1024-column LUT
+//    slice; mu = 8, fp32 LUT entries, 128 tables x 256 entries = 128 KB of
+//    shared memory per slice, stored interleaved so that entry k of the table
+//    used by lane l at chunk step j lives at
 //        LUT + (j>>1)*64KB + k*256 + (32*(j&1) + l)*4
 //    -> every lookup instruction of a warp hits 32 distinct banks whatever the
 //    keys are (bank = lane), and key -> address is ONE byte permute (PRMT)
 //    because the LUT sits on a 64 KB boundary of the shared window;
-//  * the weight is one slice-major record stream (layout.cuh); one thread
-//    keeps a bulk L2 prefetch (TMA engine, UBLKPF) several row-quad steps
-//    ahead of the warps, whose 128-bit loads (L1::no_allocate) then hit L2;
-//    a PD-deep register ring overlaps those loads with the lookups;
+//  * the weight is one slice-major record stream (layout.cuh) read with
+//    128-bit loads (L1::no_allocate) through running pointers in a ring of
+//    PD + 1 register buffers (loads issued before the lookups of the quad they
+//    overtake), no predicates in the steady state;
 //  * the activation slice is staged into shared memory by the bulk-copy
-//    (TMA) engine, double-buffered one segment ahead;
+//    (TMA) engine after the programmatic-dependent-launch wait;
 //  * lookups summed and scaled with packed f32x2 adds/FMAs (FADD2/FFMA2),
 //    two rows per instruction;
 //  * per-row partials reduced across lanes by a 6-shuffle transpose-reduce and
-//    written to an fp32 split-K workspace; a small second kernel, chained by
-//    programmatic dependent launch (PDL), sums the slices in fixed order
-//    (deterministic) and rounds y to fp16.  The LUT kernel streams its first
-//    weights before griddepcontrol.wait, so back-to-back products overlap.
+//    written to an fp32 split-K workspace; the cross-slice sum runs in the same
+//    kernel (arrival-ordered, fixed slice order: deterministic);
+//  * batched (2 <= b <= 32): vector table slots of V batch rows read with
+//    LDS.128 / LDS.64 (see the batched section).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -97,21 +96,18 @@ __device__ __forceinline__ void build_table_part(uint32_t tbl, const __half* xc,
 
 // Lookup of key byte J of word w: PRMT places the byte in bits 8..15 next to
 // the lane constant lc = LUT[31:16] | (4l+128) << 8 | 4l.
-// MODE != 0 are measurement variants (tools/kernel_probe): 1 = no LDS.
-template <int J, int MODE = 0>
+template <int J>
 __device__ __forceinline__ float lut1(uint32_t w, uint32_t lc) {
   constexpr uint32_t kSel = ((J & 1) ? 0x7605u : 0x7604u) | ((uint32_t)J << 4);
-  if (MODE == 1) return __uint_as_float(prmt<kSel>(w, lc) & 0x3fffffffu);
   return lds_f32<(J >> 1) * 65536>(prmt<kSel>(w, lc));
 }
 
 // sum over the 4 keys of word wa (row a) and of word wb (row b), as the pair (a, b)
-template <int MODE = 0>
 __device__ __forceinline__ f32x2 lut4x2(uint32_t wa, uint32_t wb, uint32_t lc) {
-  const f32x2 p0 = pack2(lut1<0, MODE>(wa, lc), lut1<0, MODE>(wb, lc));
-  const f32x2 p1 = pack2(lut1<1, MODE>(wa, lc), lut1<1, MODE>(wb, lc));
-  const f32x2 p2 = pack2(lut1<2, MODE>(wa, lc), lut1<2, MODE>(wb, lc));
-  const f32x2 p3 = pack2(lut1<3, MODE>(wa, lc), lut1<3, MODE>(wb, lc));
+  const f32x2 p0 = pack2(lut1<0>(wa, lc), lut1<0>(wb, lc));
+  const f32x2 p1 = pack2(lut1<1>(wa, lc), lut1<1>(wb, lc));
+  const f32x2 p2 = pack2(lut1<2>(wa, lc), lut1<2>(wb, lc));
+  const f32x2 p3 = pack2(lut1<3>(wa, lc), lut1<3>(wb, lc));
   return add2(add2(p0, p1), add2(p2, p3));
 }
 
@@ -186,87 +182,34 @@ __device__ __forceinline__ LaneAddr lane_addr(const Shape& sh, const uint8_t* da
   return a;
 }
 
-// L2 prefetch of row quads [a, b) of slice s (all regions), issued by one thread
-__device__ __forceinline__ void prefetch_quads(const Shape& sh, const uint8_t* data, int s, int Ls, int a, int b) {
-  if (b <= a) return;
-  const uint32_t kb = keys_bytes(sh, Ls), ab = alpha_bytes(sh, Ls), zb = z_bytes(sh, Ls);
-  // region starts are 256-aligned; per-quad sizes are multiples of 8, so round the ranges to 16 bytes
-  auto pf = [](const uint8_t* base, size_t lo, size_t hi) {
-    lo &= ~(size_t)15;
-    hi = (hi + 15) & ~(size_t)15;
-    if (hi > lo) bulk_prefetch_l2(base + lo, (uint32_t)(hi - lo));
-  };
-  pf(data + keys_base(sh, s, Ls), (size_t)a * kb, (size_t)b * kb);
-  pf(data + alpha_base(sh, s, Ls), (size_t)a * ab, (size_t)b * ab);
-  if (zb) pf(data + z_base(sh, s, Ls), (size_t)a * zb, (size_t)b * zb);
-}
-
-template <int QT, int ZM, int MODE = 0>
-__device__ __forceinline__ void ring_load(Ring<QT>& r, bool ok, const LaneAddr& la, int rq, int q) {
-  constexpr bool HAS_Z = ZM != 0, CMP = ZM == 2;  // z term; compact scales (alpha_i = 2^(i-1) s)
-  if (ok) {
-    const uint8_t* kp = la.kp + (size_t)rq * la.KB;
-    const uint8_t* ap = la.ap + (size_t)rq * la.AB;
-#pragma unroll
-    for (int i = 0; i < QT; ++i) {
-      if (QT <= 4 || i < q) {
-        if (MODE == 5) r.k[i] = ldg_stream_u4_256(kp + i * la.kstride);
-        else r.k[i] = ldg_stream_u4(kp + i * la.kstride);
-        if (MODE != 4 && (!CMP || i == 0)) r.a[i] = ldg_nc_u2(ap + 8 * i);
-        else r.a[i] = make_uint2(0, 0);
-      }
-    }
-    if (HAS_Z) r.z = ldg_nc_u2(la.zp + (size_t)rq * la.ZB);
-  } else {
-#pragma unroll
-    for (int i = 0; i < QT; ++i) {
-      r.k[i] = make_uint4(0, 0, 0, 0);
-      r.a[i] = make_uint2(0, 0);
-    }
-    r.z = make_uint2(0, 0);
-  }
-}
-
-// (acc01, acc23) (+)= sum_i alpha_i[r] * (LUT partial of row r, plane i) (+ z[r] * xsum)
-template <int QT, int ZM, int MODE = 0>
+// (acc01, acc23) = sum_i alpha_i[r] * (LUT partial of row r, plane i) (+ z[r] * xsum);
+// compact format: (sum_i 2^(i-1) partial_i) * s
+template <int QT, int ZM>
 __device__ __forceinline__ void ring_compute(const Ring<QT>& r, uint32_t lc, float xsum, f32x2& acc01, f32x2& acc23,
-                                             int q, bool accumulate) {
-  constexpr bool HAS_Z = ZM != 0, CMP = ZM == 2;  // z term; compact scales (alpha_i = 2^(i-1) s)
-  if (MODE == 3 || MODE == 4) {  // measurement variants: consume the loaded words with minimal work
-    uint32_t v = 0;
-#pragma unroll
-    for (int i = 0; i < QT; ++i) v ^= r.k[i].x ^ r.k[i].y ^ r.k[i].z ^ r.k[i].w ^ r.a[i].x ^ r.a[i].y;
-    acc01 = pack2(__uint_as_float(v & 0x3fffffffu), 0.f);
-    acc23 = pack2(0.f, 0.f);
-    return;
-  }
-  if (CMP) {  // P = sum_i 2^(i-1) (plane i partial) exactly scaled, then one multiply by s (App. C)
+                                             int q) {
+  constexpr bool HAS_Z = ZM != 0, CMP = ZM == 2;
+  if (CMP) {  // exact power-of-two plane weights, then one multiply by s (App. C)
     f32x2 p01 = 0ull, p23 = 0ull;
 #pragma unroll
     for (int i = 0; i < QT; ++i) {
       if (QT <= 4 || i < q) {
         const float w2 = (float)(1 << i) * 0.5f;
         const f32x2 ww = pack2(w2, w2);
-        p01 = fma2(ww, lut4x2<MODE>(r.k[i].x, r.k[i].y, lc), p01);
-        p23 = fma2(ww, lut4x2<MODE>(r.k[i].z, r.k[i].w, lc), p23);
+        p01 = fma2(ww, lut4x2(r.k[i].x, r.k[i].y, lc), p01);
+        p23 = fma2(ww, lut4x2(r.k[i].z, r.k[i].w, lc), p23);
       }
     }
-    const f32x2 s01 = h2_to_f32x2(r.a[0].x), s23 = h2_to_f32x2(r.a[0].y);
-    acc01 = accumulate ? fma2(s01, p01, acc01) : mul2(s01, p01);
-    acc23 = accumulate ? fma2(s23, p23, acc23) : mul2(s23, p23);
-  }
+    acc01 = mul2(h2_to_f32x2(r.a[0].x), p01);
+    acc23 = mul2(h2_to_f32x2(r.a[0].y), p23);
+  } else {
 #pragma unroll
-  for (int i = 0; i < QT; ++i) {
-    if (!CMP && (QT <= 4 || i < q)) {
-      const f32x2 a01 = h2_to_f32x2(r.a[i].x), a23 = h2_to_f32x2(r.a[i].y);
-      const f32x2 s01 = lut4x2<MODE>(r.k[i].x, r.k[i].y, lc);
-      const f32x2 s23 = lut4x2<MODE>(r.k[i].z, r.k[i].w, lc);
-      if (i == 0 && !accumulate) {
-        acc01 = mul2(a01, s01);
-        acc23 = mul2(a23, s23);
-      } else {
-        acc01 = fma2(a01, s01, acc01);
-        acc23 = fma2(a23, s23, acc23);
+    for (int i = 0; i < QT; ++i) {
+      if (QT <= 4 || i < q) {
+        const f32x2 a01 = h2_to_f32x2(r.a[i].x), a23 = h2_to_f32x2(r.a[i].y);
+        const f32x2 s01 = lut4x2(r.k[i].x, r.k[i].y, lc);
+        const f32x2 s23 = lut4x2(r.k[i].z, r.k[i].w, lc);
+        acc01 = i == 0 ? mul2(a01, s01) : fma2(a01, s01, acc01);
+        acc23 = i == 0 ? mul2(a23, s23) : fma2(a23, s23, acc23);
       }
     }
   }
@@ -287,21 +230,21 @@ __device__ __forceinline__ float lane_xsum(uint32_t lut, int lane) {
 // ---------------------------------------------------------------------------
 // GEMV, b = 1 (the paper's single-batch case)
 //
-// Work distribution: the S*RQ (slice, row-quad) items are split into equal
-// contiguous ranges, one per CTA (a range spans at most a few slices, so a CTA
-// builds few LUTs).  Inside a range the 16 warps take row quads round-robin.
+// Work distribution.  Fused mode (p.fused_J = J > 0, grid S*J <= #SMs): CTA c
+// owns slice c / J and row-quad group c % J; the cross-slice reduction runs in
+// the kernel (arrival-ordered, below).  Otherwise the S*RQ (slice, row-quad)
+// items are split into equal contiguous ranges, one per CTA (a range spans at
+// most a few slices), and lut_reduce_kernel follows.  Inside a segment the 16
+// warps take row quads rq_a + warp + 16 t round-robin.
 // ---------------------------------------------------------------------------
-template <int QT, int ZM, int PD, int MODE = 0>
+template <int QT, int ZM, int PD>
 __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) {
   constexpr bool HAS_Z = ZM != 0, CMP = ZM == 2;
-  constexpr bool RUNPTR = MODE == 7;  // running load pointers, clamped loads, branch-free steady state
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(kFull, tid >> 5, 0);  // warp-uniform for the compiler
   const Shape sh = p.sh;
   const int q = QT <= 4 ? QT : sh.q;
-  // work: a contiguous range of the S*RQ (slice, row-quad) items; in the fused
-  // mode CTA c owns slice c / J, row-quad group c % J (one segment)
   const int J = p.fused_J;
   long long it0, it1;
   if (J > 0) {
@@ -318,19 +261,15 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     trace[7] = smid();
   }
   if (it0 >= it1 && J == 0) return;
+  // fused mode: the next kernel may launch at once -- its CTAs take SMs as this
+  // grid's CTAs exit and stream their first weights before their own PDL wait
+  if (J > 0) pdl_launch_dependents();
 
   const SmemMap sm = map_smem(smem);
   __half* xbuf0 = reinterpret_cast<__half*>(sm.misc_p);
   __half* xbuf1 = reinterpret_cast<__half*>(sm.misc_p + 2048);
   const uint32_t bar0 = sm.misc + 4096, bar1 = sm.misc + 4104;
   const uint32_t lc = (sm.lut & 0xFFFF0000u) | ((uint32_t)(4 * lane + 128) << 8) | (uint32_t)(4 * lane);
-  const int pf_steps = p.pf_steps;
-
-  // last-arriver reduction (p.last_red): the next kernel may launch right away;
-  // its CTAs take SMs as soon as this grid's CTAs exit and stream their first
-  // weights before their own PDL wait
-  const bool last_red = J > 0 && p.last_red;
-  if (last_red) pdl_launch_dependents();
   if (tid == 0) {
     mbar_init(bar0, 1);
     mbar_init(bar1, 1);
@@ -338,6 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
   }
   __syncthreads();
 
+  constexpr int NB = PD + 1;  // ring of quad buffers: the load of quad t + PD is issued before quad t is computed
   int e = 0;
   long long it = it0;
   while (it < it1) {
@@ -348,64 +288,51 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     const int Ls = slice_lanes(sh.n, s);
     const bool lane_ok = lane < Ls;
     const LaneAddr la = lane_addr(sh, p.data, s, Ls, lane_ok ? lane : 0);
-
-    // 1. the x slice of the first segment (after the PDL wait: x belongs to the
-    //    preceding kernel until it completes) is requested before anything
-    //    else, so it is not queued behind the weight stream; then an L2
-    //    prefetch of the first weight steps and the register ring
     // this warp's row quads in the segment: rq_a + warp + 16 t, t < nt
     const int nt = rq_a + warp < rq_b ? (rq_b - (rq_a + warp) + kWarps - 1) / kWarps : 0;
-    // a ring of NB = PD + 1 single-quad buffers: the load for quad t + PD is
-    // issued BEFORE quad t is computed (the lookups and the reduction's
-    // shuffles would otherwise delay it), so PD quads are always in flight
-    constexpr int NB = PD + 1;
-    Ring<QT> buf[NB];
-    // RUNPTR: the warp's next quad to load is at (lk, lal, lz); each load
-    // advances them by 16 quads unless it was the warp's last quad, so a load
-    // never leaves the warp's range (quads past the end re-read the last one
-    // and are not computed) and needs no predicate or zero-fill
+    // The warp's next quad to load is at (lk, lal, lz); each load advances them
+    // by 16 quads unless it was the warp's last, so a load never leaves the
+    // warp's range (quads past the end re-read the last one and are not
+    // computed) and needs no predicate or zero-fill: the steady-state loop has
+    // no branch.  Tail-slice lanes (lane >= Ls) read lane 0's words and are
+    // zeroed before the reduction.
     const uint8_t* lk = la.kp + (size_t)(rq_a + warp) * la.KB;
     const uint8_t* lal = la.ap + (size_t)(rq_a + warp) * la.AB;
     const uint8_t* lz = la.zp + (size_t)(rq_a + warp) * la.ZB;
     int tl = 0;
-    auto load_quad = [&](Ring<QT>& b, int t) {
-      if constexpr (RUNPTR) {
-        if (nt == 0) return;  // a warp without quads in the segment loads nothing (its first quad is past the range)
+    Ring<QT> buf[NB];
+    auto load_quad = [&](Ring<QT>& b) {
+      if (nt == 0) return;  // a warp without quads in the segment loads nothing
 #pragma unroll
-        for (int i = 0; i < QT; ++i) {
-          if (QT <= 4 || i < q) {
-            b.k[i] = ldg_stream_u4(lk + i * la.kstride);
-            if (!CMP || i == 0) b.a[i] = ldg_nc_u2(lal + 8 * i);
-          }
+      for (int i = 0; i < QT; ++i) {
+        if (QT <= 4 || i < q) {
+          b.k[i] = ldg_stream_u4(lk + i * la.kstride);
+          if (!CMP || i == 0) b.a[i] = ldg_nc_u2(lal + 8 * i);
         }
-        if (HAS_Z) b.z = ldg_nc_u2(lz);
-        if (++tl < nt) {
-          lk += (size_t)kWarps * la.KB;
-          lal += (size_t)kWarps * la.AB;
-          if (HAS_Z) lz += (size_t)kWarps * la.ZB;
-        }
-      } else {
-        ring_load<QT, ZM, MODE>(b, lane_ok && t < nt, la, rq_a + warp + kWarps * t, q);
+      }
+      if (HAS_Z) b.z = ldg_nc_u2(lz);
+      if (++tl < nt) {
+        lk += (size_t)kWarps * la.KB;
+        lal += (size_t)kWarps * la.AB;
+        if (HAS_Z) lz += (size_t)kWarps * la.ZB;
       }
     };
-    const bool early = e == 0 && last_red;
-    if (early) {  // weights only: legal before the PDL wait
-#pragma unroll
-      for (int d = 0; d < PD; ++d) load_quad(buf[d], d);
-    }
+
+    // 1. fused mode, first segment: the first PD quads of every warp (weights
+    //    only: legal before the PDL wait), then the wait; x (written by the
+    //    preceding kernel) is staged by the bulk-copy engine right after it
     if (e == 0) {
-      // weights of the steps after the register prologue into L2 while the
-      // preceding kernel drains (a plain prefetch: legal before the PDL wait)
-      if (tid == 0 && p.pf_init > PD)
-        prefetch_quads(sh, p.data, s, Ls, min(rq_b, rq_a + PD * kWarps), min(rq_b, rq_a + p.pf_init * kWarps));
+      if (J > 0) {
+#pragma unroll
+        for (int d = 0; d < PD; ++d) load_quad(buf[d]);
+      }
       pdl_wait();
       if (trace) trace[5] = globaltimer_ns();
       if (warp == 0) stage_x(xbuf0, bar0, p.x, sh.n, s * kSliceCols, Ls, 32, 1, 1, lane);
     }
-    if (tid == 0 && pf_steps > 0) prefetch_quads(sh, p.data, s, Ls, rq_a, min(rq_b, rq_a + pf_steps * kWarps));
-    if (!early) {
+    if (e > 0 || J == 0) {
 #pragma unroll
-      for (int d = 0; d < PD; ++d) load_quad(buf[d], d);
+      for (int d = 0; d < PD; ++d) load_quad(buf[d]);
     }
     if (e == 0) __syncthreads();  // the zero-fill of the x buffer is visible
     // 2. wait for the staged x slice and build the 128 LUTs of the slice
@@ -425,94 +352,60 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
               slice_lanes(sh.n, sn), 32, 1, 1, lane);
     }
     const float xsum = (HAS_Z && lane_ok) ? lane_xsum(sm.lut, lane) : 0.f;
-    float* part = p.partial + (size_t)s * sh.m4;
-    // 4. main loop
-    if constexpr (RUNPTR) {
-      float* pw = part + 4 * (rq_a + warp) + (lane >> 3);  // this warp's next partial
-      auto quad = [&](const Ring<QT>& b) {
-        f32x2 acc01, acc23;
-        ring_compute<QT, ZM, 0>(b, lc, xsum, acc01, acc23, q, false);
-        if (Ls < kLanesPerSlice && !lane_ok) acc01 = acc23 = 0ull;  // tail-slice lanes loaded lane 0's words
-        const float v = reduce4(acc01, acc23, lane);
-        if ((lane & 7) == 0) *pw = v;
-        pw += 4 * kWarps;
-      };
-      int t0 = 0;
-      for (; t0 + NB <= nt; t0 += NB) {
-#pragma unroll
-        for (int d = 0; d < NB; ++d) {
-          load_quad(buf[(d + PD) % NB], 0);
-          quad(buf[d]);
-        }
-      }
-#pragma unroll
-      for (int d = 0; d < NB - 1; ++d)
-        if (t0 + d < nt) quad(buf[d]);
-    } else
-    for (int t0 = 0; t0 < nt; t0 += NB) {
-      if (tid == 0 && pf_steps > 0) {  // optional L2 prefetch pf_steps steps ahead of warp 0
-        const int lo = rq_a + kWarps * (t0 + pf_steps);
-        prefetch_quads(sh, p.data, s, Ls, lo, min(rq_b, lo + NB * kWarps));
-      }
+    // 4. main loop: per quad and plane 16 PRMT + 16 LDS + 6 FADD2 + 2 FFMA2, then
+    //    a 6-shuffle transpose-reduce and one store per row of the slice partial
+    float* pw = p.partial + (size_t)s * sh.m4 + 4 * (rq_a + warp) + (lane >> 3);  // this warp's next partial
+    auto quad = [&](const Ring<QT>& b) {
+      f32x2 acc01, acc23;
+      ring_compute<QT, ZM>(b, lc, xsum, acc01, acc23, q);
+      if (Ls < kLanesPerSlice && !lane_ok) acc01 = acc23 = 0ull;
+      const float v = reduce4(acc01, acc23, lane);
+      if ((lane & 7) == 0) *pw = v;
+      pw += 4 * kWarps;
+    };
+    int t0 = 0;
+    for (; t0 + NB <= nt; t0 += NB) {
 #pragma unroll
       for (int d = 0; d < NB; ++d) {
-        const int t = t0 + d;
-        if (t < nt) {
-          load_quad(buf[(d + PD) % NB], t + PD);
-          const int rq = rq_a + warp + kWarps * t;
-          f32x2 acc01, acc23;
-          ring_compute<QT, ZM, MODE>(buf[d], lc, xsum, acc01, acc23, q, false);
-          const float v = reduce4(acc01, acc23, lane);
-          if ((lane & 7) == 0) part[4 * rq + (lane >> 3)] = v;
-        }
+        load_quad(buf[(d + PD) % NB]);
+        quad(buf[d]);
       }
     }
+#pragma unroll
+    for (int d = 0; d < NB - 1; ++d)
+      if (t0 + d < nt) quad(buf[d]);
     if (trace && e == 0) trace[3] = globaltimer_ns();  // warp 0's loop end
-    if (J > 0 && !last_red) {  // fused mode: each warp publishes its partials with one release increment
-      __syncwarp();
-      if (lane == 0) red_release_add_u32(p.counters + blockIdx.x % J, 1u);
-    }
     __syncthreads();  // the LUT and x buffer are reused by the next segment
     if (trace) trace[e == 0 ? 4 : 6] = globaltimer_ns();  // all warps done
     it = itn;
     ++e;
   }
   if (trace) trace[7] |= (unsigned long long)e << 32;  // segments processed
-  if (last_red) {
-    // Arrival-ordered reduction: the S CTAs of row-quad group fj count in; the
-    // first S - R to arrive exit at once (their SMs go to the next kernel, which
-    // streams its first weights before its own PDL wait), the last R wait for
-    // the group and each sums 1/R of its rows over the S slices in slice order
-    // (deterministic, R11).  R = p.last_red (1 <= R <= S).
+  if (J > 0) {
+    // Fused cross-slice reduction, arrival-ordered: the S CTAs of row-quad
+    // group fj count in with one acq_rel atomic; the first S - R to arrive exit
+    // at once (their SMs go to the next kernel), the last R wait for the group
+    // and each sums 1/R of its rows over the S slices in slice order
+    // (deterministic, R11).  R = p.reducers (1 <= R <= S).
     __shared__ unsigned s_k;
     const int fj = blockIdx.x % J;
-    const int R = min(p.last_red, sh.S);
+    const int R = max(1, min(p.reducers, sh.S));
     unsigned* arrive = p.counters + fj;
     unsigned* depart = p.counters + kFusedMaxJ + fj;
-    if (e == 0) pdl_wait();  // an empty range never waited: the counters belong to the preceding kernel
-    __syncthreads();         // all partial stores of this CTA are issued
+    __syncthreads();  // all partial stores of this CTA are issued
     if (tid == 0) {
       // release: the CTA's partial stores (ordered before by the barrier) are
       // visible to whoever acquires the count; acquire: the last arriver sees all
-      if (p.xmode == 23) {
-        __threadfence();
-        s_k = atomicAdd(arrive, 1u);
-      } else {
-        s_k = atom_add_acq_rel_u32(arrive, 1u);
-      }
+      s_k = atom_add_acq_rel_u32(arrive, 1u);
     }
     __syncthreads();
     const int k = (int)s_k;
     if (k < sh.S - R) return;
-    if (tid == 0) {
-      if (k != sh.S - 1) {
-        while (ld_acquire_u32(arrive) < (unsigned)sh.S) __nanosleep(32);
-      } else if (p.xmode == 23) {
-        __threadfence();
-      }
+    if (tid == 0 && k != sh.S - 1) {
+      while (ld_acquire_u32(arrive) < (unsigned)sh.S) __nanosleep(32);
     }
     __syncthreads();
-    if (trace) trace[5] = globaltimer_ns();
+    if (trace) trace[5] = globaltimer_ns();  // (re-used) the group is complete
     const int ri = k - (sh.S - R);
     const int g0 = (int)((long long)sh.RQ * fj / J), g1 = (int)((long long)sh.RQ * (fj + 1) / J);
     const int r0 = 4 * (g0 + (int)((long long)(g1 - g0) * ri / R));
@@ -520,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     for (int r = r0 + tid; r < r1; r += kThreads) {
       float v = 0.f;
       const float* pp = p.partial + r;
-      for (int ss0 = 0; ss0 < sh.S; ss0 += 16) {
+      for (int ss0 = 0; ss0 < sh.S; ss0 += 16) {  // up to 16 slices per L2 round trip
         float t[16];
 #pragma unroll
         for (int kk = 0; kk < 16; ++kk) t[kk] = (ss0 + kk < sh.S) ? __ldcg(pp + (size_t)(ss0 + kk) * sh.m4) : 0.f;
@@ -536,51 +429,10 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
       *arrive = 0u;
       *depart = 0u;
     }
-    if (trace) trace[6] = globaltimer_ns();
+    if (trace) trace[6] = globaltimer_ns();  // reduction share done
     return;
   }
-  if (J > 0) {
-    // Fused cross-slice reduction: the S CTAs that share row-quad group fj
-    // (one per slice) meet at a counter -- all CTAs of the grid are resident
-    // (grid <= #SMs, one CTA per SM) -- then each sums its 1/S share of the
-    // group's rows over the S slices in slice order (deterministic, R11).
-    const int fs = blockIdx.x / J, fj = blockIdx.x % J;
-    unsigned* arrive = p.counters + fj;
-    unsigned* depart = p.counters + kFusedMaxJ + fj;
-    if (e == 0) {  // an empty range never reached the wait and the warp increments above
-      pdl_wait();
-      if (lane == 0) red_release_add_u32(arrive, 1u);
-    }
-    if (tid == 0) {  // all 16 warps of all S CTAs of the group have published their partials
-      while (ld_acquire_u32(arrive) < (unsigned)(sh.S * kWarps)) __nanosleep(32);
-    }
-    __syncthreads();
-    if (trace) trace[5] = globaltimer_ns();  // (re-used) the group is complete
-    const int g0 = (int)((long long)sh.RQ * fj / J), g1 = (int)((long long)sh.RQ * (fj + 1) / J);
-    const int r0 = 4 * (g0 + (int)((long long)(g1 - g0) * fs / sh.S));
-    const int r1 = min(sh.m, 4 * (g0 + (int)((long long)(g1 - g0) * (fs + 1) / sh.S)));
-    for (int r = r0 + tid; r < r1; r += kThreads) {
-      float v = 0.f;
-      const float* pp = p.partial + r;
-      for (int ss0 = 0; ss0 < sh.S; ss0 += 16) {  // up to 16 slices per L2 round trip
-        float t[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) t[k] = (ss0 + k < sh.S) ? __ldcg(pp + (size_t)(ss0 + k) * sh.m4) : 0.f;
-#pragma unroll
-        for (int k = 0; k < 16; ++k)
-          if (ss0 + k < sh.S) v += t[k];
-      }
-      if (p.yf) p.yf[r] = v;
-      else p.y[r] = __float2half_rn(v);
-    }
-    __syncthreads();
-    if (tid == 0 && atomicAdd(depart, 1u) == (unsigned)sh.S - 1) {  // the last one resets the pair
-      *arrive = 0u;
-      *depart = 0u;
-    }
-    if (trace) trace[6] = globaltimer_ns();  // reduction share done
-  }
-  pdl_launch_dependents();  // the next kernel may now be scheduled
+  pdl_launch_dependents();  // the reduction kernel may now be scheduled
 }
 
 // ---------------------------------------------------------------------------
@@ -1064,7 +916,7 @@ static cudaError_t launch(K kernel, int grid, const KParams& p, cudaStream_t st,
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = st;
   cfg.attrs = &g_pdl_attr;
-  cfg.numAttrs = p.xmode == 3 ? 0 : 1;  // experiment 3: no PDL
+  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, p);
 }
 
@@ -1083,7 +935,7 @@ static cudaError_t launch_reduce(const KParams& p, cudaStream_t st) {
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
   cfg.attrs = &g_pdl_attr;
-  cfg.numAttrs = p.xmode == 3 ? 0 : 1;
+  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, lut_reduce_kernel, (const float*)p.partial, p.sh.S, p.b, p.sh.m, p.sh.m4, p.y,
                             p.yf, p.counters);
 }
@@ -1092,25 +944,7 @@ template <int QT, int ZM>
 static cudaError_t launch_gemv_t(const KParams& p, int grid, cudaStream_t st) {
   // quads in flight per warp while one is computed (ring of PD + 1 buffers)
   constexpr int PD = QT <= 1 ? 6 : (QT <= 2 ? 4 : (QT <= 4 ? 2 : 1));
-  if constexpr (QT == 3 && ZM == 0) {
-    if (p.xmode >= 10) {  // measurement variants (LUTGEMM_XMODE)
-    switch (p.xmode) {
-      case 10: return launch(lut_gemv_kernel<QT, ZM, 1, 0>, grid, p, st);
-      case 11: return launch(lut_gemv_kernel<QT, ZM, 2, 1>, grid, p, st);
-      case 13: return launch(lut_gemv_kernel<QT, ZM, 2, 3>, grid, p, st);
-      case 16: return launch(lut_gemv_kernel<QT, ZM, 2, 4>, grid, p, st);
-      case 14: return launch(lut_gemv_kernel<QT, ZM, 3, 0>, grid, p, st);
-      case 18: return launch(lut_gemv_kernel<QT, ZM, 4, 0>, grid, p, st);
-      case 15: return launch(lut_gemv_kernel<QT, ZM, 2, 5>, grid, p, st);
-      case 19: return launch(lut_gemv_kernel<QT, ZM, 3, 5>, grid, p, st);
-      case 20: return launch(lut_gemv_kernel<QT, ZM, 2, 7>, grid, p, st);
-      case 21: return launch(lut_gemv_kernel<QT, ZM, 3, 7>, grid, p, st);
-      default: break;
-    }
-    }
-  }
-  if (p.xmode == 22) return launch(lut_gemv_kernel<QT, ZM, PD, 0>, grid, p, st);  // predicated per-quad loads (old)
-  return launch(lut_gemv_kernel<QT, ZM, PD, 7>, grid, p, st);
+  return launch(lut_gemv_kernel<QT, ZM, PD>, grid, p, st);
 }
 
 // batched: V-wide slots (V = 2 only for b = 2); p.qpw = row quads per work item
@@ -1199,7 +1033,6 @@ size_t workspace_bytes(const Shape& sh, int b) {
   return counters_bytes(sh) + ((size_t)sh.S * (size_t)batch_pad(b) * (size_t)sh.m4 * 4u + 255) / 256 * 256;
 }
 
-static int g_pf_steps = -1;
 static unsigned long long* g_trace = nullptr;
 static bool g_trace_on = false;
 constexpr int kTraceMaxCtas = 1024;
@@ -1222,10 +1055,6 @@ size_t trace_read(unsigned long long* host, size_t n) {
 
 cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, int b, uint16_t* y, float* yf,
                         void* ws, cudaStream_t st) {
-  if (g_pf_steps < 0) {
-    const char* env = getenv("LUTGEMM_PF_STEPS");  // tuning knob (default kPfSteps)
-    g_pf_steps = env ? atoi(env) : 0;
-  }
   KParams p;
   p.data = static_cast<const uint8_t*>(data);
   p.x = reinterpret_cast<const __half*>(x);
@@ -1246,19 +1075,6 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
     while (gs < 5 && (32 << gs) < sh.g) ++gs;
     p.gsh = sh.g <= kSliceCols ? gs : 31;
   }
-  p.pf_steps = g_pf_steps;
-  {
-    static int pf_init = -1;
-    if (pf_init < 0) {
-      const char* env = getenv("LUTGEMM_PF_INIT");  // tuning knob
-      pf_init = env ? atoi(env) : 0;
-    }
-    p.pf_init = pf_init;
-  }
-  {
-    const char* env = getenv("LUTGEMM_XMODE");  // experiment knob
-    p.xmode = env ? atoi(env) : 0;
-  }
   {
     static unsigned seq = 0;  // consecutive launches alternate between two halves of the trace buffer
     p.trace = g_trace_on ? g_trace + (size_t)(seq++ & 1u) * (kTraceMaxCtas / 2) * kTraceSlots : nullptr;
@@ -1273,30 +1089,26 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
   int grid = (int)std::min<long long>((long long)num_sms(), p.items);
   // fused mode (b = 1): whole slices per CTA group, S*J CTAs with J per slice,
   // when that idles at most 8 % of the SMs; the reduction then runs in-kernel
+  // with R reducers per row-quad group (~16 KB of partials each; the others
+  // exit early).  LUTGEMM_GEMV_REDUCERS overrides R (tests, tuning).
   p.fused_J = 0;
-  p.last_red = 0;
-  if (!batched && p.xmode != 4) {
+  p.reducers = 0;
+  if (!batched) {
     const int sms = num_sms();
     const int J = sh.S <= sms ? sms / sh.S : 0;
     if (J >= 1 && J <= kFusedMaxJ && sh.S <= kFusedMaxJ && sh.S * J * 100 >= sms * 92 && sh.RQ >= J) {
       p.fused_J = J;
       grid = sh.S * J;
-      // small reductions (<= 64 KB of partials per row-quad group): the last CTA
-      // of a group reduces it alone and the others exit early (the next kernel
-      // starts streaming on their SMs); large ones keep the parallel group barrier
       const long long red_bytes = (long long)sh.S * 16 * ((sh.RQ + J - 1) / J);
-      p.last_red = (int)std::min<long long>(sh.S, (red_bytes + 16383) / 16384);  // ~16 KB of partials per reducer
-      if (p.xmode == 40) p.last_red = 1;       // one reducer per group
-      if (p.xmode == 41) p.last_red = sh.S;    // every CTA of the group reduces (early trigger kept)
-      if (p.xmode == 42) p.last_red = 0;       // group barrier, trigger at the end
-      if (p.xmode >= 43 && p.xmode <= 48) p.last_red = 1 << (p.xmode - 43);  // R = 1, 2, 4, .., 32
+      p.reducers = (int)std::min<long long>(sh.S, (red_bytes + 16383) / 16384);
+      const char* env = getenv("LUTGEMM_GEMV_REDUCERS");
+      if (env && atoi(env) > 0) p.reducers = std::min(atoi(env), sh.S);
     }
   }
   cudaError_t e = sh.compact ? dispatch_q<2>(p, grid, st, batched)
                              : (sh.has_z ? dispatch_q<1>(p, grid, st, batched) : dispatch_q<0>(p, grid, st, batched));
   if (e != cudaSuccess) return e;
   if (p.fused_J > 0) return cudaSuccess;  // reduced in-kernel
-  if (p.xmode == 2) return cudaSuccess;  // experiment: no reduction (wrong results, timing only)
   return batched ? launch_reduce_batched(p, st) : launch_reduce(p, st);
 }
 

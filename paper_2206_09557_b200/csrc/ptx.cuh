@@ -53,10 +53,6 @@ __device__ __forceinline__ void sts_b64x2(uint32_t addr, unsigned long long a, u
   asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(addr), "l"(a), "l"(b) : "memory");
 }
 
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-
 __device__ __forceinline__ uint32_t ldg_nc_u32(const void* p) {
   uint32_t r;
   asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(r) : "l"(p));
@@ -68,31 +64,16 @@ __device__ __forceinline__ uint32_t ldg_nc_u16(const void* p) {
   return r;
 }
 
-// Streaming 128-bit load of packed bit-planes: read once, do not pollute L1.
-// No L2 sector-promotion hint: records are not 256-byte aligned, and a
-// .L2::256B promotion of a misaligned 512-byte warp access over-fetches DRAM.
+// Streaming 128-bit load of packed bit-planes: read once, do not pollute L1
+// (an L2::256B promotion hint measured neutral: regions are 256-byte aligned).
 __device__ __forceinline__ uint4 ldg_stream_u4(const void* p) {
   uint4 r;
-#ifdef LUTGEMM_L2_256B
-  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-#else
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
-#endif
   return r;
 }
 
-// as ldg_stream_u4 with the L2 256-byte sector-promotion hint (regions are 256-byte aligned)
-__device__ __forceinline__ uint4 ldg_stream_u4_256(const void* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
 __device__ __forceinline__ uint2 ldg_nc_u2(const void* p) {
   uint2 r;
   asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
@@ -169,12 +150,6 @@ __device__ __forceinline__ uint32_t smid() {
   uint32_t r;
   asm volatile("mov.u32 %0, %smid;" : "=r"(r));
   return r;
-}
-
-// Bulk L2 prefetch of [p, p+bytes) by the TMA engine (SASS UBLKPF); p and
-// bytes must be multiples of 16.
-__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
 __device__ __forceinline__ float2 h2_to_f2(uint32_t u) {

@@ -266,21 +266,23 @@ def test_uniform_compact_full_parity(b, m, n, q, g):
     assert np.array_equal(run(wc, (2 * X.astype(np.float32)).astype(np.float16), f32=True), 2 * yf)
 
 
-@pytest.mark.parametrize("xmode", ["40", "42"])
+@pytest.mark.parametrize("reducers", ["1", "64"])
 @pytest.mark.parametrize("m,n,q,g,off", [(6000, 4096, 3, 128, False), (2049, 12288, 4, 64, True)])
-def test_gemv_reduction_modes(monkeypatch, xmode, m, n, q, g, off):
-    """Both fused cross-slice reductions of the GEMV -- last-arriving CTA per
-    row group (40) and the parallel group barrier (42) -- agree with the oracle
-    and with each other bit for bit (same fixed slice order, R11)."""
+def test_gemv_reduction_modes(monkeypatch, reducers, m, n, q, g, off):
+    """The fused cross-slice reduction with one reducer per row group and with
+    every CTA of the group reducing agrees with the oracle, and the two agree bit
+    for bit (same fixed slice order, R11) -- whatever the arrival order."""
     d = gen_bcq(m + q, m, n, q, g, offset=off)
     X = gen_x(n, 1, n)
     w = pack(d)
-    monkeypatch.setenv("LUTGEMM_XMODE", xmode)
+    monkeypatch.setenv("LUTGEMM_GEMV_REDUCERS", reducers)
     y = run(w, X, f32=True)
-    monkeypatch.setenv("LUTGEMM_XMODE", "42" if xmode == "40" else "40")
+    for _ in range(3):
+        assert np.array_equal(run(w, X, f32=True), y)
+    monkeypatch.setenv("LUTGEMM_GEMV_REDUCERS", "64" if reducers == "1" else "1")
     assert np.array_equal(run(w, X, f32=True), y)
-    monkeypatch.delenv("LUTGEMM_XMODE")
-    assert_parity(y, O.bcq_gemv(d["planes"], d["alpha"], d["offset"], X, n, g), (m, n, q, g, xmode))
+    monkeypatch.delenv("LUTGEMM_GEMV_REDUCERS")
+    assert_parity(y, O.bcq_gemv(d["planes"], d["alpha"], d["offset"], X, n, g), (m, n, q, g, reducers))
 
 
 def _random_configs(k=24, seed=2206):
