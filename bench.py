@@ -162,6 +162,16 @@ def load_traffic_profile(kernel: str):
 # CPU oracle timing (cpu_baseline leg and --impl reference)
 # ---------------------------------------------------------------------------
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def time_oracle(cfg: dict, budget_s: float, min_rows: int = 64, rows_cap: int | None = None):
     """Time the fp64 oracle on a bounded row sample of cfg's layer.
     Returns (GB/s of algorithmic bytes, seconds, rows, threads)."""
@@ -227,7 +237,8 @@ def run_reference(args, cfg) -> None:
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["name"], "m": m, "n": n, "q": q, "g": g, "b": 1, "rows_per_step": rows},
-        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -311,11 +322,15 @@ def run_gpu(args, cfg) -> None:
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(local)
     barrier()
+    # events between consecutive graph replays (no gap: recorded on the same stream)
+    rep_ev = [torch.cuda.Event(enable_timing=True) for _ in range((reps if use_graph else 0) + 1)]
     with sampler:
         t_start.record(stream)
         if use_graph:
-            for _ in range(reps):
+            rep_ev[0].record(stream)
+            for r in range(reps):
                 graph.replay()
+                rep_ev[r + 1].record(stream)
         else:
             for i in range(args.steps):
                 step(i)
@@ -323,6 +338,11 @@ def run_gpu(args, cfg) -> None:
         torch.cuda.synchronize()
     barrier()
     total_ms = t_start.elapsed_time(t_end)
+    dist = None
+    if use_graph and reps >= 3:
+        per = np.array([rep_ev[r].elapsed_time(rep_ev[r + 1]) for r in range(reps)]) / G * 1e3  # us per GEMV
+        dist = {"p10": round(float(np.percentile(per, 10)), 3), "median": round(float(np.median(per)), 3),
+                "p90": round(float(np.percentile(per, 90)), 3), "replays": int(reps), "gemvs_per_replay": int(G)}
     # per-launch events on the launching stream (one GEMV = one LUT kernel with the fused reduction)
     ne = min(args.steps, 200)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(ne)]
@@ -376,7 +396,8 @@ def run_gpu(args, cfg) -> None:
     if rank == 0 and world == 1 and not args.no_cpu:
         gbs, secs, rows, threads = time_oracle(cfg, budget_s=args.cpu_budget)
         cpu = {"value": round(gbs, 5), "unit": UNIT, "cores": threads, "kind": "oracle",
-               "sample": f"fp64 numpy oracle on the first {rows} of {m} rows of {cfg['name']} ({secs:.1f} s)"}
+               "sample": f"fp64 numpy oracle on the first {rows} of {m} rows of {cfg['name']} ({secs:.1f} s)",
+               "cpu_model": cpu_model()}
 
     box = box_copy_gbs(dev) if rank == 0 else None
     if rank == 0:
@@ -393,6 +414,7 @@ def run_gpu(args, cfg) -> None:
                        "l2": f"{ncopies} rotating weight copies = {ncopies * B / 1e6:.0f} MB > 3x L2 ({l2 / 1e6:.0f} MB)",
                        "bytes_alg_per_gemv": B},
             "us_per_gemv": round(ms_per_step * 1e3, 3),
+            "us_per_gemv_dist": dist,
             "pct_of_peak_hbm": round(100 * value / world / peaks["hbm_gbs"], 2),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": load_traffic_profile(kname),
