@@ -808,6 +808,218 @@ __global__ void __launch_bounds__(NTH, 1) lut_gemm_batched_kernel(const KParams 
   pdl_launch_dependents();
 }
 
+// ---------------------------------------------------------------------------
+// b = 2 with the GEMV's streaming structure.  A 512-column half slice
+// (hs = 2 s + h: layout lanes [16h, 16h+16) of layout slice s) holds the LUTs of
+// BOTH activation rows: 64 chunks x 256 keys x 2 rows = 128 KB, read with one
+// PRMT + LDS.64 per key (vector slots, V = 2, of the batched section).  Lane
+// l = qi * 16 + w owns quad qi of a pair of consecutive row quads, word w; a
+// warp step is one quad pair.  Unlike the batched kernel there are no
+// accumulators across LUT rebuilds: each quad's 4 rows x 2 batch partials are
+// reduced over the 16 w lanes right away (8-value transpose-reduce, 8
+// shuffles) and stored as a half-slice partial, so registers go to a PD-deep
+// load ring as in the GEMV; the cross-half-slice sum is the GEMV's fused
+// arrival-ordered reduction (or lut_reduce_kernel when not fused).
+// Partials [S2][2][m4], S2 = half slices.
+// ---------------------------------------------------------------------------
+
+// (row rho, batch) pairs of one quad, reduced over the 16 lanes sharing qi:
+// returns the sum for (row (lane >> 2) & 3, batch (lane >> 1) & 1), valid in even lanes
+__device__ __forceinline__ float reduce8x16(const f32x2 (&acc)[4][1], int lane) {
+  float2 v[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) v[r] = unpack2(acc[r][0]);
+  // xor 8: keep rows {0,1} (bit3 = 0) or {2,3}
+  const bool b3 = lane & 8;
+  float k0x = b3 ? v[2].x : v[0].x, k0y = b3 ? v[2].y : v[0].y, k1x = b3 ? v[3].x : v[1].x, k1y = b3 ? v[3].y : v[1].y;
+  const float s0x = b3 ? v[0].x : v[2].x, s0y = b3 ? v[0].y : v[2].y, s1x = b3 ? v[1].x : v[3].x, s1y = b3 ? v[1].y : v[3].y;
+  k0x += __shfl_xor_sync(kFull, s0x, 8);
+  k0y += __shfl_xor_sync(kFull, s0y, 8);
+  k1x += __shfl_xor_sync(kFull, s1x, 8);
+  k1y += __shfl_xor_sync(kFull, s1y, 8);
+  // xor 4: keep row (bit2 ? second : first) of the pair
+  const bool b2 = lane & 4;
+  float kx = b2 ? k1x : k0x, ky = b2 ? k1y : k0y;
+  const float sx = b2 ? k0x : k1x, sy = b2 ? k0y : k1y;
+  kx += __shfl_xor_sync(kFull, sx, 4);
+  ky += __shfl_xor_sync(kFull, sy, 4);
+  // xor 2: keep batch (bit1 ? 1 : 0)
+  const bool b1 = lane & 2;
+  float k = b1 ? ky : kx;
+  k += __shfl_xor_sync(kFull, b1 ? kx : ky, 2);
+  k += __shfl_xor_sync(kFull, k, 1);
+  return k;
+}
+
+template <int QT, int ZM, int PD>
+__global__ void __launch_bounds__(kThreads, 1) lut_gemv2_kernel(const KParams p) {
+  constexpr bool HAS_Z = ZM != 0, CMP = ZM == 2;
+  constexpr int NB = PD + 1;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(kFull, tid >> 5, 0);
+  const int qi = lane >> 4, w = lane & 15;
+  const Shape sh = p.sh;
+  const int q = QT <= 4 ? QT : sh.q;
+  const int NP2 = (sh.RQ + 1) / 2;  // quad pairs
+  const int S2 = p.s2;              // half slices
+  const int J = p.fused_J;
+  long long it0, it1;  // items = (half slice, quad pair)
+  if (J > 0) {
+    const int fs = blockIdx.x / J, fj = blockIdx.x % J;
+    it0 = (long long)fs * NP2 + (long long)NP2 * fj / J;
+    it1 = (long long)fs * NP2 + (long long)NP2 * (fj + 1) / J;
+  } else {
+    it0 = p.items * blockIdx.x / gridDim.x;
+    it1 = p.items * (blockIdx.x + 1) / gridDim.x;
+  }
+  if (it0 >= it1 && J == 0) return;
+  if (J > 0) pdl_launch_dependents();
+
+  const SmemMap sm = map_smem(smem);
+  const uint32_t xt0 = sm.misc, xt1 = sm.misc + 2048;
+  const __half* xtile0 = reinterpret_cast<const __half*>(sm.misc_p);
+  const __half* xtile1 = reinterpret_cast<const __half*>(sm.misc_p + 2048);
+  const uint32_t lc = (sm.lut & 0xFFFF0000u) | ((uint32_t)((16 + w) * 8) << 8) | (uint32_t)(w * 8);
+  // x tile of half slice hs: rows 0, 1 of x, 512 columns, in the vector-slot cell order (xcell<2>)
+  auto load_x = [&](uint32_t dst, int hs) {
+    if (tid < 128) {
+      const int s = hs >> 1, h = hs & 1;
+      const int Lh = min(16, slice_lanes(sh.n, s) - 16 * h);
+      const int bt = tid >> 6, c = tid & 63;  // row, 16-byte cell of the row (8 columns)
+      const bool ok = c / 4 < Lh;
+      const __half* src = ok ? p.x + (size_t)bt * sh.n + s * kSliceCols + 512 * h + 8 * c : p.x;
+      cp_async_16(dst + 16u * (uint32_t)xcell<2>(c, bt, 1), src, ok ? 16u : 0u);
+    }
+  };
+
+  int e = 0;
+  long long it = it0;
+  while (it < it1) {
+    const int hs = (int)(it / NP2);
+    const int pa = (int)(it % NP2);
+    const int pb = (int)min((long long)NP2, (long long)pa + (it1 - it));
+    const long long itn = it + (pb - pa);
+    const int s = hs >> 1, h = hs & 1;
+    const int Ls = slice_lanes(sh.n, s);
+    const int Lh = min(16, Ls - 16 * h);
+    const bool lane_ok = w < Lh;
+    const LaneAddr la = lane_addr(sh, p.data, s, Ls, 16 * h + (lane_ok ? w : 0));
+    // this warp's pairs pa + warp + 16 t, t < nt; the lane's quad 2 pair + qi exists for t < ntl
+    const int nt = pa + warp < pb ? (pb - (pa + warp) + kWarps - 1) / kWarps : 0;
+    const int last_quad = 2 * (pa + warp + kWarps * (nt - 1)) + qi;
+    const int ntl = nt - (nt > 0 && last_quad >= sh.RQ ? 1 : 0);
+    const int rq0 = 2 * (pa + warp) + qi;
+    const uint8_t* lk = la.kp + (size_t)rq0 * la.KB;
+    const uint8_t* lal = la.ap + (size_t)rq0 * la.AB;
+    const uint8_t* lz = la.zp + (size_t)rq0 * la.ZB;
+    int tl = 0;
+    VRing<QT> buf[NB];
+    auto load_pair = [&](VRing<QT>& b) {
+      if (ntl <= 0) return;  // nothing valid for this lane: no loads (its first quad is past the range)
+#pragma unroll
+      for (int i = 0; i < QT; ++i) {
+        if (QT <= 4 || i < q) {
+          b.k[i] = ldg_stream_u4(lk + i * la.kstride);
+          if (!CMP || i == 0) b.a[i] = ldg_nc_u2(lal + 8 * i);
+        }
+      }
+      if (HAS_Z) b.z = ldg_nc_u2(lz);
+      if (++tl < ntl) {
+        lk += (size_t)(2 * kWarps) * la.KB;
+        lal += (size_t)(2 * kWarps) * la.AB;
+        if (HAS_Z) lz += (size_t)(2 * kWarps) * la.ZB;
+      }
+    };
+    if (e == 0) {
+      if (J > 0) {
+#pragma unroll
+        for (int d = 0; d < PD; ++d) load_pair(buf[d]);
+      }
+      pdl_wait();
+      load_x(xt0, hs);
+    }
+    if (e > 0 || J == 0) {
+#pragma unroll
+      for (int d = 0; d < PD; ++d) load_pair(buf[d]);
+    }
+    cp_async_wait_all();
+    __syncthreads();  // the x tile is visible
+    build_vtables<2, kThreads>(sm.lut, (e & 1) ? xtile1 : xtile0, 1, tid);
+    __syncthreads();
+    if (itn < it1) load_x((e & 1) ? xt0 : xt1, (int)(itn / NP2));  // lands during the lookups
+    f32x2 xs[1];
+    if (HAS_Z) vword<2>(0xFFFFFFFFu, lc, xs);  // sum of x (both rows) over the lane's 32 columns
+    float* pw = p.partial + (size_t)hs * 2 * sh.m4 + 4 * rq0;
+    const int store_off = ((lane >> 1) & 1) * sh.m4 + ((lane >> 2) & 3);  // (batch, row) of the even lanes
+    auto pair = [&](const VRing<QT>& b, bool valid) {
+      f32x2 acc[4][1] = {{0ull}, {0ull}, {0ull}, {0ull}};
+      vring_compute<2, QT, ZM>(b, lc, xs, acc, q);
+      if (!valid || (Lh < 16 && !lane_ok)) acc[0][0] = acc[1][0] = acc[2][0] = acc[3][0] = 0ull;
+      const float v = reduce8x16(acc, lane);
+      if (valid && (lane & 1) == 0) pw[store_off] = v;
+      pw += 4 * 2 * kWarps;
+    };
+    int t0 = 0;
+    for (; t0 + NB <= nt; t0 += NB) {
+#pragma unroll
+      for (int d = 0; d < NB; ++d) {
+        load_pair(buf[(d + PD) % NB]);
+        pair(buf[d], t0 + d < ntl);
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < NB - 1; ++d)
+      if (t0 + d < nt) pair(buf[d], t0 + d < ntl);
+    __syncthreads();  // the LUT and x tile are reused by the next segment
+    it = itn;
+    ++e;
+  }
+  if (J > 0) {  // fused arrival-ordered reduction over the S2 half slices (as in lut_gemv_kernel)
+    __shared__ unsigned s_k;
+    const int fj = blockIdx.x % J;
+    const int R = max(1, min(p.reducers, S2));
+    unsigned* arrive = p.counters + fj;
+    unsigned* depart = p.counters + kFusedMaxJ + fj;
+    __syncthreads();
+    if (tid == 0) s_k = atom_add_acq_rel_u32(arrive, 1u);
+    __syncthreads();
+    const int k = (int)s_k;
+    if (k < S2 - R) return;
+    if (tid == 0 && k != S2 - 1) {
+      while (ld_acquire_u32(arrive) < (unsigned)S2) __nanosleep(32);
+    }
+    __syncthreads();
+    const int ri = k - (S2 - R);
+    const int g0 = 2 * (int)((long long)NP2 * fj / J), g1 = min(sh.RQ, 2 * (int)((long long)NP2 * (fj + 1) / J));
+    const int r0 = 4 * (g0 + (int)((long long)(g1 - g0) * ri / R));
+    const int r1 = min(sh.m, 4 * (g0 + (int)((long long)(g1 - g0) * (ri + 1) / R)));
+    for (int idx = tid; idx < 2 * (r1 - r0); idx += kThreads) {
+      const int beta = idx / (r1 - r0), r = r0 + idx % (r1 - r0);
+      float v = 0.f;
+      const float* pp = p.partial + (size_t)beta * sh.m4 + r;
+      for (int ss0 = 0; ss0 < S2; ss0 += 16) {
+        float t[16];
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk)
+          t[kk] = (ss0 + kk < S2) ? __ldcg(pp + (size_t)(ss0 + kk) * 2 * sh.m4) : 0.f;
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk)
+          if (ss0 + kk < S2) v += t[kk];
+      }
+      if (p.yf) p.yf[(size_t)beta * sh.m + r] = v;
+      else p.y[(size_t)beta * sh.m + r] = __float2half_rn(v);
+    }
+    __syncthreads();
+    if (tid == 0 && atomicAdd(depart, 1u) == (unsigned)R - 1) {
+      *arrive = 0u;
+      *depart = 0u;
+    }
+    return;
+  }
+  pdl_launch_dependents();
+}
+
 // Batched cross-slice reduction: Y[beta][r] = sum_{s<S2} partial[s][r][beta]
 // in slice order (deterministic, R11), fp16 RNE (or fp32).  A block owns 64
 // rows: coalesced reads of the [row][b_pad] partials, transposed in shared
@@ -947,6 +1159,12 @@ static cudaError_t launch_gemv_t(const KParams& p, int grid, cudaStream_t st) {
   return launch(lut_gemv_kernel<QT, ZM, PD>, grid, p, st);
 }
 
+template <int QT, int ZM>
+static cudaError_t launch_gemv2_t(const KParams& p, int grid, cudaStream_t st) {
+  constexpr int PD = QT <= 2 ? 3 : (QT <= 4 ? 2 : 1);
+  return launch(lut_gemv2_kernel<QT, ZM, PD>, grid, p, st);
+}
+
 // batched: V-wide slots (V = 2 only for b = 2); p.qpw = row quads per work item
 // (256 or 128).  V = 2 runs 16 warps (128 registers: 4 rows x 2 batch x 16
 // quads of accumulators), V = 4 and q > 4 run 8 warps (255 registers).
@@ -965,6 +1183,7 @@ static cudaError_t launch_batched_v(const KParams& p, int grid, cudaStream_t st)
 
 template <int QT, int ZM>
 static cudaError_t launch_batched_t(const KParams& p, int grid, cudaStream_t st) {
+  if (p.b == 2 && p.s2 > 0) return launch_gemv2_t<QT, ZM>(p, grid, st);
   return p.b == 2 ? launch_batched_v<2, QT, ZM>(p, grid, st) : launch_batched_v<4, QT, ZM>(p, grid, st);
 }
 
@@ -1030,7 +1249,8 @@ int batch_pad(int b) {
 }
 
 size_t workspace_bytes(const Shape& sh, int b) {
-  return counters_bytes(sh) + ((size_t)sh.S * (size_t)batch_pad(b) * (size_t)sh.m4 * 4u + 255) / 256 * 256;
+  const size_t slices = b == 2 ? 2 * (size_t)sh.S : (size_t)sh.S;  // b = 2: half-slice partials
+  return counters_bytes(sh) + (slices * (size_t)batch_pad(b) * (size_t)sh.m4 * 4u + 255) / 256 * 256;
 }
 
 static unsigned long long* g_trace = nullptr;
@@ -1051,6 +1271,13 @@ size_t trace_read(unsigned long long* host, size_t n) {
   if (n > cap) n = cap;
   cudaMemcpy(host, g_trace, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   return n;
+}
+
+// fused mode of the GEMV-structured kernels: S slices x J CTAs with J = #SMs / S,
+// idling at most 8 % of the SMs, and at least J row units per slice
+static bool fusable(int S, int units, int sms) {
+  const int J = S <= sms ? sms / S : 0;
+  return J >= 1 && J <= kFusedMaxJ && S <= kFusedMaxJ && S * J * 100 >= sms * 92 && units >= J;
 }
 
 cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, int b, uint16_t* y, float* yf,
@@ -1080,8 +1307,14 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
     p.trace = g_trace_on ? g_trace + (size_t)(seq++ & 1u) * (kTraceMaxCtas / 2) * kTraceSlots : nullptr;
   }
   const bool batched = b > 1;
+  p.s2 = 0;
   if (!batched) {
     p.items = (long long)sh.S * sh.RQ;
+  } else if (b == 2 && !(getenv("LUTGEMM_B2_BATCHED") && atoi(getenv("LUTGEMM_B2_BATCHED")))) {
+    // b = 2: GEMV-structured kernel over 512-column half slices (LUTGEMM_B2_BATCHED=1
+    // selects the vector-slot batched kernel instead, for comparison)
+    p.s2 = (sh.n + 511) / 512;
+    p.items = (long long)p.s2 * ((sh.RQ + 1) / 2);
   } else {
     p.spi = 0;
     plan_batched(sh, num_sms(), p);
@@ -1093,10 +1326,21 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
   // exit early).  LUTGEMM_GEMV_REDUCERS overrides R (tests, tuning).
   p.fused_J = 0;
   p.reducers = 0;
+  if (p.s2 > 0) {  // b = 2 kernel: the GEMV's fused mode over half slices
+    const int sms = num_sms();
+    const int NP2 = (sh.RQ + 1) / 2;
+    const int J = p.s2 <= sms ? sms / p.s2 : 0;
+    if (fusable(p.s2, NP2, sms)) {
+      p.fused_J = J;
+      grid = p.s2 * J;
+      const long long red_bytes = (long long)p.s2 * 2 * 4 * 8 * ((NP2 + J - 1) / J);
+      p.reducers = (int)std::min<long long>(p.s2, (red_bytes + 16383) / 16384);
+    }
+  }
   if (!batched) {
     const int sms = num_sms();
     const int J = sh.S <= sms ? sms / sh.S : 0;
-    if (J >= 1 && J <= kFusedMaxJ && sh.S <= kFusedMaxJ && sh.S * J * 100 >= sms * 92 && sh.RQ >= J) {
+    if (fusable(sh.S, sh.RQ, sms)) {
       p.fused_J = J;
       grid = sh.S * J;
       const long long red_bytes = (long long)sh.S * 16 * ((sh.RQ + J - 1) / J);
@@ -1109,6 +1353,11 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
                              : (sh.has_z ? dispatch_q<1>(p, grid, st, batched) : dispatch_q<0>(p, grid, st, batched));
   if (e != cudaSuccess) return e;
   if (p.fused_J > 0) return cudaSuccess;  // reduced in-kernel
+  if (p.s2 > 0) {  // half-slice partials [S2][2][m4]: the GEMV reduction kernel with S = S2
+    KParams r = p;
+    r.sh.S = p.s2;
+    return launch_reduce(r, st);
+  }
   return batched ? launch_reduce_batched(p, st) : launch_reduce(p, st);
 }
 
