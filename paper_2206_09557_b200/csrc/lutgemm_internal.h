@@ -26,7 +26,7 @@ struct KParams {
   int gsh;           // batched: layout lane -> slice-local group shift (31: one group per slice)
   int fused_J;       // GEMV: CTAs per slice in the fused-reduction mode (0: separate reduction kernel)
   int reducers;      // GEMV fused mode: the last R CTAs to arrive in a row-quad group reduce it
-  int s2;            // b = 2 GEMV-structured kernel: number of 512-column half slices (0: not used)
+  int s2;            // b <= 4 GEMV-structured kernel: number of sub-slices (0: not used)
   long long items;
   unsigned long long* trace;  // optional per-CTA timeline (kTraceSlots u64 per CTA), or null
 };

@@ -809,27 +809,27 @@ __global__ void __launch_bounds__(NTH, 1) lut_gemm_batched_kernel(const KParams 
 }
 
 // ---------------------------------------------------------------------------
-// b = 2 with the GEMV's streaming structure.  A 512-column half slice
-// (hs = 2 s + h: layout lanes [16h, 16h+16) of layout slice s) holds the LUTs of
-// BOTH activation rows: 64 chunks x 256 keys x 2 rows = 128 KB, read with one
-// PRMT + LDS.64 per key (vector slots, V = 2, of the batched section).  Lane
-// l = qi * 16 + w owns quad qi of a pair of consecutive row quads, word w; a
-// warp step is one quad pair.  Unlike the batched kernel there are no
-// accumulators across LUT rebuilds: each quad's 4 rows x 2 batch partials are
-// reduced over the 16 w lanes right away (8-value transpose-reduce, 8
-// shuffles) and stored as a half-slice partial, so registers go to a PD-deep
-// load ring as in the GEMV; the cross-half-slice sum is the GEMV's fused
-// arrival-ordered reduction (or lut_reduce_kernel when not fused).
-// Partials [S2][2][m4], S2 = half slices.
+// b <= 4 with the GEMV's streaming structure.  With V = 2 (b = 2) or V = 4
+// (b = 3, 4) a sub-slice of 1024 / V columns (layout lanes [LR h, LR h + LR) of a
+// slice, LR = 32 / V; sub-slice hs = V s + h) holds the LUTs of all V
+// activation rows: 32 LR... = 128 KB of V-float vector slots (the batched
+// kernel's slot layout with NV = 1), read with one PRMT + LDS.64 / LDS.128 per
+// key.  Lane l = qi * LR + w owns quad qi of a group of V consecutive row quads
+// and word w; a warp step is one quad group.  Unlike the batched kernel there
+// are no accumulators across LUT rebuilds: each quad's 4 rows x V partials are
+// reduced over its LR lanes right away (transpose-reduce) and stored as a
+// sub-slice partial, so registers go to a PD-deep load ring as in the GEMV; the
+// cross-sub-slice sum is the GEMV's fused arrival-ordered reduction (or
+// lut_reduce_kernel when the sub-slices outnumber the SMs).
+// Partials [SV][b][m4], SV = sub-slices.
 // ---------------------------------------------------------------------------
 
-// (row rho, batch) pairs of one quad, reduced over the 16 lanes sharing qi:
-// returns the sum for (row (lane >> 2) & 3, batch (lane >> 1) & 1), valid in even lanes
-__device__ __forceinline__ float reduce8x16(const f32x2 (&acc)[4][1], int lane) {
+// V = 2: the 4 rows x 2 batch sums of a quad over the 16 lanes sharing qi;
+// lane keeps (row (lane >> 2) & 3, batch (lane >> 1) & 1), valid in even lanes
+__device__ __forceinline__ void reduce_quad(const f32x2 (&acc)[4][1], int lane, float (&out)[1]) {
   float2 v[4];
 #pragma unroll
   for (int r = 0; r < 4; ++r) v[r] = unpack2(acc[r][0]);
-  // xor 8: keep rows {0,1} (bit3 = 0) or {2,3}
   const bool b3 = lane & 8;
   float k0x = b3 ? v[2].x : v[0].x, k0y = b3 ? v[2].y : v[0].y, k1x = b3 ? v[3].x : v[1].x, k1y = b3 ? v[3].y : v[1].y;
   const float s0x = b3 ? v[0].x : v[2].x, s0y = b3 ? v[0].y : v[2].y, s1x = b3 ? v[1].x : v[3].x, s1y = b3 ? v[1].y : v[3].y;
@@ -837,38 +837,67 @@ __device__ __forceinline__ float reduce8x16(const f32x2 (&acc)[4][1], int lane) 
   k0y += __shfl_xor_sync(kFull, s0y, 8);
   k1x += __shfl_xor_sync(kFull, s1x, 8);
   k1y += __shfl_xor_sync(kFull, s1y, 8);
-  // xor 4: keep row (bit2 ? second : first) of the pair
   const bool b2 = lane & 4;
   float kx = b2 ? k1x : k0x, ky = b2 ? k1y : k0y;
   const float sx = b2 ? k0x : k1x, sy = b2 ? k0y : k1y;
   kx += __shfl_xor_sync(kFull, sx, 4);
   ky += __shfl_xor_sync(kFull, sy, 4);
-  // xor 2: keep batch (bit1 ? 1 : 0)
   const bool b1 = lane & 2;
   float k = b1 ? ky : kx;
   k += __shfl_xor_sync(kFull, b1 ? kx : ky, 2);
   k += __shfl_xor_sync(kFull, k, 1);
-  return k;
+  out[0] = k;
 }
 
-template <int QT, int ZM, int PD>
-__global__ void __launch_bounds__(kThreads, 1) lut_gemv2_kernel(const KParams p) {
+// V = 4: the 4 rows x 4 batch sums of a quad over the 8 lanes sharing qi; lane
+// keeps row 2 (lane >> 2 & 1) + (lane >> 1 & 1), batch pair (lane & 1) (two values)
+__device__ __forceinline__ void reduce_quad(const f32x2 (&acc)[4][2], int lane, float (&out)[2]) {
+  const bool b2 = lane & 4, b1 = lane & 2, b0 = lane & 1;
+  // xor 4: keep rows {0,1} or {2,3} (8 values)
+  f32x2 k[2][2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const f32x2 keep = b2 ? acc[2 + r][p] : acc[r][p], send = b2 ? acc[r][p] : acc[2 + r][p];
+      const float2 sv = unpack2(send);
+      k[r][p] = add2(keep, pack2(__shfl_xor_sync(kFull, sv.x, 4), __shfl_xor_sync(kFull, sv.y, 4)));
+    }
+  // xor 2: keep one row of the pair (4 values)
+  f32x2 m[2];
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const f32x2 keep = b1 ? k[1][p] : k[0][p], send = b1 ? k[0][p] : k[1][p];
+    const float2 sv = unpack2(send);
+    m[p] = add2(keep, pack2(__shfl_xor_sync(kFull, sv.x, 2), __shfl_xor_sync(kFull, sv.y, 2)));
+  }
+  // xor 1: keep batch pair (0,1) or (2,3) (2 values)
+  const f32x2 keep = b0 ? m[1] : m[0], send = b0 ? m[0] : m[1];
+  const float2 sv = unpack2(send);
+  const float2 r = unpack2(add2(keep, pack2(__shfl_xor_sync(kFull, sv.x, 1), __shfl_xor_sync(kFull, sv.y, 1))));
+  out[0] = r.x;
+  out[1] = r.y;
+}
+
+template <int V, int QT, int ZM, int PD>
+__global__ void __launch_bounds__(kThreads, 1) lut_gemvv_kernel(const KParams p) {
   constexpr bool HAS_Z = ZM != 0, CMP = ZM == 2;
-  constexpr int NB = PD + 1;
+  constexpr int NB = PD + 1, LR = 32 / V, NP = V / 2;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(kFull, tid >> 5, 0);
-  const int qi = lane >> 4, w = lane & 15;
+  const int qi = lane / LR, w = lane % LR;
   const Shape sh = p.sh;
   const int q = QT <= 4 ? QT : sh.q;
-  const int NP2 = (sh.RQ + 1) / 2;  // quad pairs
-  const int S2 = p.s2;              // half slices
+  const int b = p.b;
+  const int NG = (sh.RQ + V - 1) / V;  // quad groups
+  const int SV = p.s2;                 // sub-slices
   const int J = p.fused_J;
-  long long it0, it1;  // items = (half slice, quad pair)
+  long long it0, it1;  // items = (sub-slice, quad group)
   if (J > 0) {
     const int fs = blockIdx.x / J, fj = blockIdx.x % J;
-    it0 = (long long)fs * NP2 + (long long)NP2 * fj / J;
-    it1 = (long long)fs * NP2 + (long long)NP2 * (fj + 1) / J;
+    it0 = (long long)fs * NG + (long long)NG * fj / J;
+    it1 = (long long)fs * NG + (long long)NG * (fj + 1) / J;
   } else {
     it0 = p.items * blockIdx.x / gridDim.x;
     it1 = p.items * (blockIdx.x + 1) / gridDim.x;
@@ -880,132 +909,152 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv2_kernel(const KParams p)
   const uint32_t xt0 = sm.misc, xt1 = sm.misc + 2048;
   const __half* xtile0 = reinterpret_cast<const __half*>(sm.misc_p);
   const __half* xtile1 = reinterpret_cast<const __half*>(sm.misc_p + 2048);
-  const uint32_t lc = (sm.lut & 0xFFFF0000u) | ((uint32_t)((16 + w) * 8) << 8) | (uint32_t)(w * 8);
-  // x tile of half slice hs: rows 0, 1 of x, 512 columns, in the vector-slot cell order (xcell<2>)
+  const uint32_t lc = (sm.lut & 0xFFFF0000u) | ((uint32_t)((LR + w) * 4 * V) << 8) | (uint32_t)(w * 4 * V);
+  // x tile of sub-slice hs: rows 0..V-1 of x (zero for rows >= b), 32 LR columns,
+  // in the vector-slot cell order (xcell<V>, NV = 1)
   auto load_x = [&](uint32_t dst, int hs) {
     if (tid < 128) {
-      const int s = hs >> 1, h = hs & 1;
-      const int Lh = min(16, slice_lanes(sh.n, s) - 16 * h);
-      const int bt = tid >> 6, c = tid & 63;  // row, 16-byte cell of the row (8 columns)
-      const bool ok = c / 4 < Lh;
-      const __half* src = ok ? p.x + (size_t)bt * sh.n + s * kSliceCols + 512 * h + 8 * c : p.x;
-      cp_async_16(dst + 16u * (uint32_t)xcell<2>(c, bt, 1), src, ok ? 16u : 0u);
+      const int s = hs / V, h = hs % V;
+      const int Lh = min(LR, slice_lanes(sh.n, s) - LR * h);
+      const int per_row = 4 * LR;
+      const int bt = tid / per_row, c = tid % per_row;
+      const bool ok = bt < b && c / 4 < Lh;
+      const __half* src = ok ? p.x + (size_t)bt * sh.n + s * kSliceCols + 32 * LR * h + 8 * c : p.x;
+      cp_async_16(dst + 16u * (uint32_t)xcell<V>(c, bt, 1), src, ok ? 16u : 0u);
     }
   };
 
   int e = 0;
   long long it = it0;
   while (it < it1) {
-    const int hs = (int)(it / NP2);
-    const int pa = (int)(it % NP2);
-    const int pb = (int)min((long long)NP2, (long long)pa + (it1 - it));
-    const long long itn = it + (pb - pa);
-    const int s = hs >> 1, h = hs & 1;
+    const int hs = (int)(it / NG);
+    const int ga = (int)(it % NG);
+    const int gb = (int)min((long long)NG, (long long)ga + (it1 - it));
+    const long long itn = it + (gb - ga);
+    const int s = hs / V, h = hs % V;
     const int Ls = slice_lanes(sh.n, s);
-    const int Lh = min(16, Ls - 16 * h);
+    const int Lh = min(LR, Ls - LR * h);
     const bool lane_ok = w < Lh;
-    const LaneAddr la = lane_addr(sh, p.data, s, Ls, 16 * h + (lane_ok ? w : 0));
-    // this warp's pairs pa + warp + 16 t, t < nt; the lane's quad 2 pair + qi exists for t < ntl
-    const int nt = pa + warp < pb ? (pb - (pa + warp) + kWarps - 1) / kWarps : 0;
-    const int last_quad = 2 * (pa + warp + kWarps * (nt - 1)) + qi;
+    const LaneAddr la = lane_addr(sh, p.data, s, Ls, LR * h + (lane_ok ? w : 0));
+    // this warp's groups ga + warp + 16 t, t < nt; the lane's quad V group + qi exists for t < ntl
+    const int nt = ga + warp < gb ? (gb - (ga + warp) + kWarps - 1) / kWarps : 0;
+    const int last_quad = V * (ga + warp + kWarps * (nt - 1)) + qi;
     const int ntl = nt - (nt > 0 && last_quad >= sh.RQ ? 1 : 0);
-    const int rq0 = 2 * (pa + warp) + qi;
+    const int rq0 = V * (ga + warp) + qi;
     const uint8_t* lk = la.kp + (size_t)rq0 * la.KB;
     const uint8_t* lal = la.ap + (size_t)rq0 * la.AB;
     const uint8_t* lz = la.zp + (size_t)rq0 * la.ZB;
     int tl = 0;
     VRing<QT> buf[NB];
-    auto load_pair = [&](VRing<QT>& b) {
+    auto load_group = [&](VRing<QT>& bb) {
       if (ntl <= 0) return;  // nothing valid for this lane: no loads (its first quad is past the range)
 #pragma unroll
       for (int i = 0; i < QT; ++i) {
         if (QT <= 4 || i < q) {
-          b.k[i] = ldg_stream_u4(lk + i * la.kstride);
-          if (!CMP || i == 0) b.a[i] = ldg_nc_u2(lal + 8 * i);
+          bb.k[i] = ldg_stream_u4(lk + i * la.kstride);
+          if (!CMP || i == 0) bb.a[i] = ldg_nc_u2(lal + 8 * i);
         }
       }
-      if (HAS_Z) b.z = ldg_nc_u2(lz);
+      if (HAS_Z) bb.z = ldg_nc_u2(lz);
       if (++tl < ntl) {
-        lk += (size_t)(2 * kWarps) * la.KB;
-        lal += (size_t)(2 * kWarps) * la.AB;
-        if (HAS_Z) lz += (size_t)(2 * kWarps) * la.ZB;
+        lk += (size_t)(V * kWarps) * la.KB;
+        lal += (size_t)(V * kWarps) * la.AB;
+        if (HAS_Z) lz += (size_t)(V * kWarps) * la.ZB;
       }
     };
     if (e == 0) {
       if (J > 0) {
 #pragma unroll
-        for (int d = 0; d < PD; ++d) load_pair(buf[d]);
+        for (int d = 0; d < PD; ++d) load_group(buf[d]);
       }
       pdl_wait();
       load_x(xt0, hs);
     }
     if (e > 0 || J == 0) {
 #pragma unroll
-      for (int d = 0; d < PD; ++d) load_pair(buf[d]);
+      for (int d = 0; d < PD; ++d) load_group(buf[d]);
     }
     cp_async_wait_all();
     __syncthreads();  // the x tile is visible
-    build_vtables<2, kThreads>(sm.lut, (e & 1) ? xtile1 : xtile0, 1, tid);
+    build_vtables<V, kThreads>(sm.lut, (e & 1) ? xtile1 : xtile0, 1, tid);
     __syncthreads();
-    if (itn < it1) load_x((e & 1) ? xt0 : xt1, (int)(itn / NP2));  // lands during the lookups
-    f32x2 xs[1];
-    if (HAS_Z) vword<2>(0xFFFFFFFFu, lc, xs);  // sum of x (both rows) over the lane's 32 columns
-    float* pw = p.partial + (size_t)hs * 2 * sh.m4 + 4 * rq0;
-    const int store_off = ((lane >> 1) & 1) * sh.m4 + ((lane >> 2) & 3);  // (batch, row) of the even lanes
-    auto pair = [&](const VRing<QT>& b, bool valid) {
-      f32x2 acc[4][1] = {{0ull}, {0ull}, {0ull}, {0ull}};
-      vring_compute<2, QT, ZM>(b, lc, xs, acc, q);
-      if (!valid || (Lh < 16 && !lane_ok)) acc[0][0] = acc[1][0] = acc[2][0] = acc[3][0] = 0ull;
-      const float v = reduce8x16(acc, lane);
-      if (valid && (lane & 1) == 0) pw[store_off] = v;
-      pw += 4 * 2 * kWarps;
+    if (itn < it1) load_x((e & 1) ? xt0 : xt1, (int)(itn / NG));  // lands during the lookups
+    f32x2 xs[NP];
+    if (HAS_Z) vword<V>(0xFFFFFFFFu, lc, xs);  // sum of x (all rows) over the lane's 32 columns
+    // the even / all lanes of a quad store (batch, row) sums; partial [hs][beta][4 rq + row]
+    float* pw = p.partial + (size_t)hs * b * sh.m4 + 4 * rq0;
+    auto group = [&](const VRing<QT>& bb, bool valid) {
+      f32x2 acc[4][NP];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp) acc[r][pp] = 0ull;
+      vring_compute<V, QT, ZM>(bb, lc, xs, acc, q);
+      if (!valid || (Lh < LR && !lane_ok))
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int pp = 0; pp < NP; ++pp) acc[r][pp] = 0ull;
+      float out[NP];
+      reduce_quad(acc, lane, out);
+      if (valid) {
+        if constexpr (V == 2) {
+          if ((lane & 1) == 0) pw[((lane >> 1) & 1) * sh.m4 + ((lane >> 2) & 3)] = out[0];
+        } else {
+          const int row = 2 * ((lane >> 2) & 1) + ((lane >> 1) & 1), beta = 2 * (lane & 1);
+          if (beta < b) pw[beta * sh.m4 + row] = out[0];
+          if (beta + 1 < b) pw[(beta + 1) * sh.m4 + row] = out[1];
+        }
+      }
+      pw += 4 * V * kWarps;
     };
     int t0 = 0;
     for (; t0 + NB <= nt; t0 += NB) {
 #pragma unroll
       for (int d = 0; d < NB; ++d) {
-        load_pair(buf[(d + PD) % NB]);
-        pair(buf[d], t0 + d < ntl);
+        load_group(buf[(d + PD) % NB]);
+        group(buf[d], t0 + d < ntl);
       }
     }
 #pragma unroll
     for (int d = 0; d < NB - 1; ++d)
-      if (t0 + d < nt) pair(buf[d], t0 + d < ntl);
+      if (t0 + d < nt) group(buf[d], t0 + d < ntl);
     __syncthreads();  // the LUT and x tile are reused by the next segment
     it = itn;
     ++e;
   }
-  if (J > 0) {  // fused arrival-ordered reduction over the S2 half slices (as in lut_gemv_kernel)
+  if (J > 0) {  // fused arrival-ordered reduction over the SV sub-slices (as in lut_gemv_kernel)
     __shared__ unsigned s_k;
     const int fj = blockIdx.x % J;
-    const int R = max(1, min(p.reducers, S2));
+    const int R = max(1, min(p.reducers, SV));
     unsigned* arrive = p.counters + fj;
     unsigned* depart = p.counters + kFusedMaxJ + fj;
     __syncthreads();
     if (tid == 0) s_k = atom_add_acq_rel_u32(arrive, 1u);
     __syncthreads();
     const int k = (int)s_k;
-    if (k < S2 - R) return;
-    if (tid == 0 && k != S2 - 1) {
-      while (ld_acquire_u32(arrive) < (unsigned)S2) __nanosleep(32);
+    if (k < SV - R) return;
+    if (tid == 0 && k != SV - 1) {
+      while (ld_acquire_u32(arrive) < (unsigned)SV) __nanosleep(32);
     }
     __syncthreads();
-    const int ri = k - (S2 - R);
-    const int g0 = 2 * (int)((long long)NP2 * fj / J), g1 = min(sh.RQ, 2 * (int)((long long)NP2 * (fj + 1) / J));
+    const int ri = k - (SV - R);
+    const int g0 = V * (int)((long long)NG * fj / J), g1 = min(sh.RQ, V * (int)((long long)NG * (fj + 1) / J));
     const int r0 = 4 * (g0 + (int)((long long)(g1 - g0) * ri / R));
     const int r1 = min(sh.m, 4 * (g0 + (int)((long long)(g1 - g0) * (ri + 1) / R)));
-    for (int idx = tid; idx < 2 * (r1 - r0); idx += kThreads) {
-      const int beta = idx / (r1 - r0), r = r0 + idx % (r1 - r0);
+    const int nr = max(0, r1 - r0);
+    for (int idx = tid; idx < b * nr; idx += kThreads) {
+      const int beta = idx / nr, r = r0 + idx % nr;
       float v = 0.f;
       const float* pp = p.partial + (size_t)beta * sh.m4 + r;
-      for (int ss0 = 0; ss0 < S2; ss0 += 16) {
+      for (int ss0 = 0; ss0 < SV; ss0 += 16) {
         float t[16];
 #pragma unroll
         for (int kk = 0; kk < 16; ++kk)
-          t[kk] = (ss0 + kk < S2) ? __ldcg(pp + (size_t)(ss0 + kk) * 2 * sh.m4) : 0.f;
+          t[kk] = (ss0 + kk < SV) ? __ldcg(pp + (size_t)(ss0 + kk) * b * sh.m4) : 0.f;
 #pragma unroll
         for (int kk = 0; kk < 16; ++kk)
-          if (ss0 + kk < S2) v += t[kk];
+          if (ss0 + kk < SV) v += t[kk];
       }
       if (p.yf) p.yf[(size_t)beta * sh.m + r] = v;
       else p.y[(size_t)beta * sh.m + r] = __float2half_rn(v);
@@ -1160,9 +1209,10 @@ static cudaError_t launch_gemv_t(const KParams& p, int grid, cudaStream_t st) {
 }
 
 template <int QT, int ZM>
-static cudaError_t launch_gemv2_t(const KParams& p, int grid, cudaStream_t st) {
+static cudaError_t launch_gemvv_t(const KParams& p, int grid, cudaStream_t st) {
   constexpr int PD = QT <= 2 ? 3 : (QT <= 4 ? 2 : 1);
-  return launch(lut_gemv2_kernel<QT, ZM, PD>, grid, p, st);
+  if (p.b == 2) return launch(lut_gemvv_kernel<2, QT, ZM, PD>, grid, p, st);
+  return launch(lut_gemvv_kernel<4, QT, ZM, PD>, grid, p, st);
 }
 
 // batched: V-wide slots (V = 2 only for b = 2); p.qpw = row quads per work item
@@ -1183,7 +1233,7 @@ static cudaError_t launch_batched_v(const KParams& p, int grid, cudaStream_t st)
 
 template <int QT, int ZM>
 static cudaError_t launch_batched_t(const KParams& p, int grid, cudaStream_t st) {
-  if (p.b == 2 && p.s2 > 0) return launch_gemv2_t<QT, ZM>(p, grid, st);
+  if (p.s2 > 0) return launch_gemvv_t<QT, ZM>(p, grid, st);
   return p.b == 2 ? launch_batched_v<2, QT, ZM>(p, grid, st) : launch_batched_v<4, QT, ZM>(p, grid, st);
 }
 
@@ -1249,7 +1299,8 @@ int batch_pad(int b) {
 }
 
 size_t workspace_bytes(const Shape& sh, int b) {
-  const size_t slices = b == 2 ? 2 * (size_t)sh.S : (size_t)sh.S;  // b = 2: half-slice partials
+  // b <= 4: sub-slice partials of the GEMV-structured kernel ([V S][b][m4], V = 2 or 4)
+  const size_t slices = b == 2 ? 2 * (size_t)sh.S : (b <= 4 && b > 1 ? 4 * (size_t)sh.S : (size_t)sh.S);
   return counters_bytes(sh) + (slices * (size_t)batch_pad(b) * (size_t)sh.m4 * 4u + 255) / 256 * 256;
 }
 
@@ -1310,11 +1361,12 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
   p.s2 = 0;
   if (!batched) {
     p.items = (long long)sh.S * sh.RQ;
-  } else if (b == 2 && !(getenv("LUTGEMM_B2_BATCHED") && atoi(getenv("LUTGEMM_B2_BATCHED")))) {
-    // b = 2: GEMV-structured kernel over 512-column half slices (LUTGEMM_B2_BATCHED=1
-    // selects the vector-slot batched kernel instead, for comparison)
-    p.s2 = (sh.n + 511) / 512;
-    p.items = (long long)p.s2 * ((sh.RQ + 1) / 2);
+  } else if (b <= 4 && !(getenv("LUTGEMM_SMALLB_BATCHED") && atoi(getenv("LUTGEMM_SMALLB_BATCHED")))) {
+    // b <= 4: GEMV-structured kernel over sub-slices of 1024 / V columns, V = 2 (b = 2)
+    // or 4 (b = 3, 4); LUTGEMM_SMALLB_BATCHED=1 selects the vector-slot batched kernel
+    const int V = b == 2 ? 2 : 4;
+    p.s2 = (sh.n + 1024 / V - 1) / (1024 / V);
+    p.items = (long long)p.s2 * ((sh.RQ + V - 1) / V);
   } else {
     p.spi = 0;
     plan_batched(sh, num_sms(), p);
@@ -1326,14 +1378,15 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
   // exit early).  LUTGEMM_GEMV_REDUCERS overrides R (tests, tuning).
   p.fused_J = 0;
   p.reducers = 0;
-  if (p.s2 > 0) {  // b = 2 kernel: the GEMV's fused mode over half slices
+  if (p.s2 > 0) {  // b <= 4 kernel: the GEMV's fused mode over sub-slices
     const int sms = num_sms();
-    const int NP2 = (sh.RQ + 1) / 2;
+    const int V = b == 2 ? 2 : 4;
+    const int NG = (sh.RQ + V - 1) / V;
     const int J = p.s2 <= sms ? sms / p.s2 : 0;
-    if (fusable(p.s2, NP2, sms)) {
+    if (fusable(p.s2, NG, sms)) {
       p.fused_J = J;
       grid = p.s2 * J;
-      const long long red_bytes = (long long)p.s2 * 2 * 4 * 8 * ((NP2 + J - 1) / J);
+      const long long red_bytes = (long long)p.s2 * b * 4 * (4 * V) * ((NG + J - 1) / J);
       p.reducers = (int)std::min<long long>(p.s2, (red_bytes + 16383) / 16384);
     }
   }
@@ -1353,7 +1406,7 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
                              : (sh.has_z ? dispatch_q<1>(p, grid, st, batched) : dispatch_q<0>(p, grid, st, batched));
   if (e != cudaSuccess) return e;
   if (p.fused_J > 0) return cudaSuccess;  // reduced in-kernel
-  if (p.s2 > 0) {  // half-slice partials [S2][2][m4]: the GEMV reduction kernel with S = S2
+  if (p.s2 > 0) {  // sub-slice partials [SV][b][m4]: the GEMV reduction kernel with S = SV
     KParams r = p;
     r.sh.S = p.s2;
     return launch_reduce(r, st);

@@ -1,0 +1,9 @@
+set -e
+python -c "import __graft_entry__ as g; g.build()"
+set +e
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_quantize.py -m gpu -q -x 2>&1 | tail -4
+for X in 0 1; do
+echo "LUTGEMM_SMALLB_BATCHED=$X"; LUTGEMM_SMALLB_BATCHED=$X python tools/sweep.py --cases 49152:12288:3:128:2,49152:12288:3:128:3,49152:12288:3:128:4,12288:49152:3:128:4,12288:12288:3:128:4,8192:22016:4:128:4:2,22016:8192:4:128:4:2 --steps 200 | python -c "
+import sys,json
+print('   ', [ (json.loads(l)['case'][:22], json.loads(l)['us']) for l in sys.stdin])"
+done
