@@ -186,6 +186,16 @@ def main(tag, rnd="01"):
           f"{stack['ms_per_token']} ms per token ({stack['GBps_per_gpu']} GB/s over "
           f"{stack['weight_bytes_per_gpu'] / 1e9:.1f} GB of packed weights); per linear (eager): "
           f"{stack['per_linear_us_eager']}.", f"Paper context: {stack['paper_context_ms']}.", ""]
+    chk = os.path.join(PROF, f"r{rnd}_stack_tp1_check.json")
+    if os.path.exists(p("stack_check.json")):
+        d = json.loads(open(p("stack_check.json")).read().strip().splitlines()[-1])
+        json.dump(d, open(chk, "w"), indent=1)
+    if os.path.exists(chk):
+        d = json.load(open(chk))
+        v = list(d["parity_rel_l2_sampled"].values())
+        t += [f"With `--check` (`r{rnd}_stack_tp1_check.json`): {d['ms_per_token']:.2f} ms per token on that box; "
+              f"64 sampled rows of every linear of layers 0 and {d['layers'] - 1} against the fp64 oracle: rel-L2 "
+              f"{min(v):.1e} .. {max(v):.1e} (bound 2e-3).", ""]
     open(os.path.join(PROF, f"r{rnd}_sweep.md"), "w").write("\n".join(t) + "\n")
     # sanitizers (tools/sanitize.sh), if that run is present
     san = {t: os.path.join(OUT, f"sanitize_{t}.txt") for t in ("memcheck", "racecheck", "synccheck", "initcheck")}
