@@ -35,6 +35,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
+#include <utility>
+#include <vector>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -1157,6 +1160,20 @@ static int num_sms() {
   return g_num_sms[dev];
 }
 
+// the dynamic shared-memory opt-in, set once per (kernel, device) instead of on every launch
+static cudaError_t ensure_smem_attr(const void* kernel) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto& d : done)
+    if (d.first == kernel && d.second == dev) return cudaSuccess;
+  const cudaError_t err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  if (err == cudaSuccess) done.emplace_back(kernel, dev);
+  return err;
+}
+
 static cudaLaunchAttribute g_pdl_attr = [] {
   cudaLaunchAttribute a;
   a.id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1169,7 +1186,7 @@ std::atomic<unsigned long long> g_launches{0};  // product kernels launched by t
 template <typename K>
 static cudaError_t launch(K kernel, int grid, const KParams& p, cudaStream_t st, int threads = kThreads) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  cudaError_t err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  cudaError_t err = ensure_smem_attr(reinterpret_cast<const void*>(kernel));
   if (err != cudaSuccess) return err;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
