@@ -556,15 +556,6 @@ __device__ __forceinline__ void build_vtables(uint32_t lut, const __half* tile, 
   }
 }
 
-// One row quad's operands for one lane: the key words of its 4 rows for q
-// planes (one 16-byte load each), their scales (4 fp16 per plane) and z.
-template <int QT>
-struct VRing {
-  uint4 k[QT];
-  uint2 a[QT];
-  uint2 z;
-};
-
 // The lane's running pointers into the three regions of one slice: plane i's
 // key words of the lane's next quad at kq + i * kstride, its scales at
 // aq + 8 i, its z at zq; each advances by V quads per step.
@@ -574,7 +565,7 @@ struct VPtr {
 };
 
 template <int QT, int ZM>
-__device__ __forceinline__ void vring_load(VRing<QT>& r, bool ok, VPtr& pt, int q) {
+__device__ __forceinline__ void vring_load(Ring<QT>& r, bool ok, VPtr& pt, int q) {
   constexpr bool HAS_Z = ZM != 0, CMP = ZM == 2;  // z term; compact scales (alpha_i = 2^(i-1) s)
 #pragma unroll
   for (int i = 0; i < QT; ++i) {
@@ -596,7 +587,7 @@ __device__ __forceinline__ void vring_load(VRing<QT>& r, bool ok, VPtr& pt, int 
 
 // acc[rho][p] (+)= sum_i alpha_i[rho] * (word lookups of row rho, plane i) + z[rho] * xsum, rho < 4
 template <int V, int QT, int ZM>
-__device__ __forceinline__ void vring_compute(const VRing<QT>& r, uint32_t lc, const f32x2 (&xs)[V / 2],
+__device__ __forceinline__ void vring_compute(const Ring<QT>& r, uint32_t lc, const f32x2 (&xs)[V / 2],
                                               f32x2 (&acc)[4][V / 2], int q) {
   constexpr bool HAS_Z = ZM != 0, CMP = ZM == 2;  // z term; compact scales (alpha_i = 2^(i-1) s)
   constexpr int NP = V / 2;
@@ -735,7 +726,7 @@ __global__ void __launch_bounds__(NTH, 1) lut_gemm_batched_kernel(const KParams 
     pt.zq = p.data + z_base(sh, st.s, Ls) + (size_t)rq * ZB + (uint32_t)(pl >> gsh) * 8u;
     return pt;
   };
-  VRing<QT> ring[NB];
+  Ring<QT> ring[NB];
   VPtr nxt;  // pointers of the next step, positioned after its prologue groups
   bool nxt_ok;
   auto prologue = [&](const VStep& st) {
@@ -948,8 +939,8 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemvv_kernel(const KParams p)
     const uint8_t* lal = la.ap + (size_t)rq0 * la.AB;
     const uint8_t* lz = la.zp + (size_t)rq0 * la.ZB;
     int tl = 0;
-    VRing<QT> buf[NB];
-    auto load_group = [&](VRing<QT>& bb) {
+    Ring<QT> buf[NB];
+    auto load_group = [&](Ring<QT>& bb) {
       if (ntl <= 0) return;  // nothing valid for this lane: no loads (its first quad is past the range)
 #pragma unroll
       for (int i = 0; i < QT; ++i) {
@@ -986,7 +977,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemvv_kernel(const KParams p)
     if (HAS_Z) vword<V>(0xFFFFFFFFu, lc, xs);  // sum of x (all rows) over the lane's 32 columns
     // the even / all lanes of a quad store (batch, row) sums; partial [hs][beta][4 rq + row]
     float* pw = p.partial + (size_t)hs * b * sh.m4 + 4 * rq0;
-    auto group = [&](const VRing<QT>& bb, bool valid) {
+    auto group = [&](const Ring<QT>& bb, bool valid) {
       f32x2 acc[4][NP];
 #pragma unroll
       for (int r = 0; r < 4; ++r)
@@ -1107,8 +1098,7 @@ __global__ void __launch_bounds__(256) lut_reduce_batched_kernel(const float* __
 // One thread per (beta, row quad); launched with PDL after the LUT kernel.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) lut_reduce_kernel(const float* __restrict__ partial, int S, int b, int m,
-                                                         int m4, __half* __restrict__ y, float* __restrict__ yf,
-                                                         unsigned* __restrict__ counters) {
+                                                         int m4, __half* __restrict__ y, float* __restrict__ yf) {
   pdl_launch_dependents();  // the next product may start streaming its weights
   pdl_wait();               // partials are complete and visible
   const int RQ = m4 / 4;
@@ -1215,7 +1205,7 @@ static cudaError_t launch_reduce(const KParams& p, cudaStream_t st) {
   cfg.attrs = &g_pdl_attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, lut_reduce_kernel, (const float*)p.partial, p.sh.S, p.b, p.sh.m, p.sh.m4, p.y,
-                            p.yf, p.counters);
+                            p.yf);
 }
 
 template <int QT, int ZM>
