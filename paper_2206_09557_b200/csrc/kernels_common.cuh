@@ -211,8 +211,9 @@ __device__ __forceinline__ float lane_xsum(uint32_t lut, int lane) {
 // across sub-slices and across the spi slices of a work item.
 //
 // Lanes: LR = 32 / V lanes form one LDS phase (8 lanes x 16 B or 16 x 8 B =
-// 128 B); lane = rg * LR + wv, wv = w * NV + v: row group rg (4 / V rows of the
-// row quad), layout lane w of the sub-slice, batch vector v (rows vV..vV+V-1).
+// 128 B); lane = qi * LR + wv, wv = w * NV + v: quad qi of a group of V
+// consecutive row quads (all 4 rows of it), layout lane w of the sub-slice,
+// batch vector v (rows vV..vV+V-1).
 // Slot of (chunk 4w + J, vector v) for key k:
 //     LUT + (J >> 1) * 64 KB + k * 256 + (LR * (J & 1) + wv) * 4V
 // The LR lanes of a phase have distinct wv, hence distinct 4V-byte bank groups
@@ -415,8 +416,8 @@ struct VStep {
 // b <= 4 with the GEMV's streaming structure.  With V = 2 (b = 2) or V = 4
 // (b = 3, 4) a sub-slice of 1024 / V columns (layout lanes [LR h, LR h + LR) of a
 // slice, LR = 32 / V; sub-slice hs = V s + h) holds the LUTs of all V
-// activation rows: 32 LR... = 128 KB of V-float vector slots (the batched
-// kernel's slot layout with NV = 1), read with one PRMT + LDS.64 / LDS.128 per
+// activation rows: 4 LR chunks x 256 keys x V floats = 128 KB of vector slots
+// (the batched kernel's slot layout with NV = 1), read with one PRMT + LDS.64 / LDS.128 per
 // key.  Lane l = qi * LR + w owns quad qi of a group of V consecutive row quads
 // and word w; a warp step is one quad group.  Unlike the batched kernel there
 // are no accumulators across LUT rebuilds: each quad's 4 rows x V partials are
