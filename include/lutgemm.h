@@ -250,6 +250,40 @@ lutgemm_status lutgemm_tp_destroy(lutgemm_tp* tp);
 int lutgemm_tp_rank(const lutgemm_tp* tp);
 int lutgemm_tp_nranks(const lutgemm_tp* tp);
 
+/* ---------------- Fused rows all-gather over peer memory ----------------
+ * The tensor-parallel GEMV of ROWS_ALLGATHER with the collective fused into the
+ * GEMV's epilogue: the reducer CTAs of rank r store each finished row of its
+ * shard straight into every rank's output buffer over NVLink / NVSwitch (CUDA
+ * IPC mappings), the grid's last reducer signals every rank at system scope,
+ * and a one-thread wait kernel on the stream acquires until the rank has all P
+ * signals of the round.  No NCCL call; one process per GPU.
+ *
+ * Each rank owns two output buffers (double buffer) and a signal counter.  The
+ * output of a call stays valid until the call after next (flow control: a rank
+ * overwrites a buffer only after every peer has signalled the round in between,
+ * which that peer does after its stream ran everything queued before it).
+ * Every rank must make the same sequence of calls.  Not CUDA-graph capturable
+ * (the buffer parity and the wait target are host-side round counts). */
+typedef struct lutgemm_p2p lutgemm_p2p;
+
+/* Allocate this rank's buffers (two of out_bytes, device) and signal counter
+ * and write a 256-byte exchange record (CUDA IPC handles, rank, sizes) that the
+ * caller gathers from all ranks, in rank order, by any transport. 1 <= nranks <= 8. */
+lutgemm_status lutgemm_p2p_create(int rank, int nranks, size_t out_bytes, lutgemm_p2p** out, uint8_t record[256]);
+/* Open the peers' buffers from the gathered records [nranks][256]. */
+lutgemm_status lutgemm_p2p_connect(lutgemm_p2p* g, const uint8_t* records);
+/* y_full [P * m_shard] (fp16) = the rows of every rank's shard times x, gathered
+ * into this rank's current output buffer, returned in *y_full (may be NULL);
+ * if y_copy (device) is not NULL the result is also copied there on `stream`.
+ * shard: this rank's rows [r m_shard, (r+1) m_shard) of W, packed; x [n] fp16
+ * (16-byte aligned); ws >= lutgemm_workspace_bytes(m_shard, n, 1).  The shard
+ * must run the fused GEMV mode (LUTGEMM_ERR_UNSUPPORTED otherwise: too few row
+ * quads for the J CTAs per slice, or more slices than SMs). */
+lutgemm_status lutgemm_p2p_gemv_allgather(lutgemm_p2p* g, const lutgemm_weight* shard, const uint16_t* x, void* ws,
+                                          size_t ws_bytes, void* stream, uint16_t** y_full, uint16_t* y_copy);
+/* Synchronises the device, closes the peer mappings and frees the buffers. */
+lutgemm_status lutgemm_p2p_destroy(lutgemm_p2p* g);
+
 #ifdef __cplusplus
 }
 #endif

@@ -9,6 +9,7 @@ from .lutgemm import (  # noqa: F401
     FMT_UNIFORM_COMPACT,
     LIB_PATH,
     LutgemmError,
+    P2PGroup,
     PackedBCQ,
     TPComm,
     TP_COLS_ALLREDUCE,

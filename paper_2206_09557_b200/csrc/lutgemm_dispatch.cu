@@ -50,7 +50,9 @@ const cudaLaunchAttribute* pdl_attr() {
 
 std::atomic<unsigned long long> g_launches{0};
 
-static size_t counters_bytes(const Shape&) { return 2u * kFusedMaxJ * 4u; }
+// arrival / departure counter pairs of the fused reduction, then the grid-wide
+// done counter of the fused rows all-gather (256-byte aligned)
+static size_t counters_bytes(const Shape&) { return 2u * kFusedMaxJ * 4u + 256u; }
 
 int batch_pad(int b) {
   int bp = 1;
@@ -91,9 +93,31 @@ static bool fusable(int S, int units, int sms) {
   return J >= 1 && J <= kFusedMaxJ && S <= kFusedMaxJ && S * J * 100 >= sms * 92 && units >= J;
 }
 
+static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint16_t* x, int b, uint16_t* y, float* yf,
+                                  void* ws, cudaStream_t st, __half* const* peer_y, unsigned* const* peer_sig,
+                                  int npeers, int yoff);
+
 cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, int b, uint16_t* y, float* yf,
                         void* ws, cudaStream_t st) {
+  return run_product_ex(sh, data, x, b, y, yf, ws, st, nullptr, nullptr, 0, 0);
+}
+
+cudaError_t run_gemv_p2p(const Shape& sh, const void* data, const uint16_t* x, void* ws, __half* const* peer_y,
+                         unsigned* const* peer_sig, int npeers, int yoff, cudaStream_t st) {
+  if (npeers < 1 || npeers > 8) return cudaErrorInvalidValue;
+  return run_product_ex(sh, data, x, 1, nullptr, nullptr, ws, st, peer_y, peer_sig, npeers, yoff);
+}
+
+static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint16_t* x, int b, uint16_t* y, float* yf,
+                                  void* ws, cudaStream_t st, __half* const* peer_y, unsigned* const* peer_sig,
+                                  int npeers, int yoff) {
   KParams p;
+  p.npeers = npeers;
+  p.yoff = yoff;
+  for (int i = 0; i < 8; ++i) {
+    p.peer_y[i] = i < npeers ? peer_y[i] : nullptr;
+    p.peer_sig[i] = i < npeers ? peer_sig[i] : nullptr;
+  }
   p.data = static_cast<const uint8_t*>(data);
   p.x = reinterpret_cast<const __half*>(x);
   p.y = reinterpret_cast<__half*>(y);
@@ -162,6 +186,7 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
       if (env && atoi(env) > 0) p.reducers = std::min(atoi(env), sh.S);
     }
   }
+  if (npeers > 0 && (batched || p.fused_J <= 0)) return cudaErrorNotSupported;  // the fused epilogue only
   cudaError_t e = !batched ? launch_gemv(p, grid, st) : (p.s2 > 0 ? launch_smallb(p, grid, st) : launch_batched(p, grid, st));
   if (e != cudaSuccess) return e;
   if (p.fused_J > 0) return cudaSuccess;  // reduced in-kernel

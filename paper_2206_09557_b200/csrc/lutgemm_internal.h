@@ -26,6 +26,11 @@ struct KParams {
   int gsh;           // batched: layout lane -> slice-local group shift (31: one group per slice)
   int fused_J;       // GEMV: CTAs per slice in the fused-reduction mode (0: separate reduction kernel)
   int reducers;      // GEMV fused mode: the last R CTAs to arrive in a row-quad group reduce it
+  // fused rows all-gather (NEXT-1): rank r's output rows go to peer_y[pr] + yoff on every rank pr
+  __half* peer_y[8];
+  unsigned* peer_sig[8];
+  int npeers;        // 0: plain output
+  int yoff;
   int s2;            // b <= 4 GEMV-structured kernel: number of sub-slices (0: not used)
   long long items;
   unsigned long long* trace;  // optional per-CTA timeline (kTraceSlots u64 per CTA), or null
@@ -47,6 +52,13 @@ int batch_pad(int b);
 // fixed-order cross-slice reduction.
 cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, int b, uint16_t* y, float* yf,
                         void* ws, cudaStream_t st);
+
+// NEXT-1: b = 1 product whose fused reduction stores the rows into every rank's
+// output (peer_y[pr] + yoff) and signals every rank (peer_sig[pr]); requires the
+// fused GEMV mode (returns cudaErrorNotSupported otherwise).  Then the wait.
+cudaError_t run_gemv_p2p(const Shape& sh, const void* data, const uint16_t* x, void* ws, __half* const* peer_y,
+                         unsigned* const* peer_sig, int npeers, int yoff, cudaStream_t st);
+cudaError_t launch_p2p_wait(const unsigned* sig, unsigned target, cudaStream_t st);
 
 cudaError_t run_pack_bcq(const Shape& sh, const uint32_t* planes, const uint16_t* alpha, const uint16_t* offset,
                          void* dst, cudaStream_t st);

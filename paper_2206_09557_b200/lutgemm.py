@@ -62,6 +62,10 @@ SIGNATURES = [
     ("lutgemm_trace_enable", _I, [_I]),
     ("lutgemm_trace_read", _SZ, [ctypes.POINTER(ctypes.c_uint64), _SZ]),
     ("lutgemm_launch_count", ctypes.c_uint64, []),
+    ("lutgemm_p2p_create", _I, [_I, _I, _SZ, ctypes.POINTER(_P), _P]),
+    ("lutgemm_p2p_connect", _I, [_P, _P]),
+    ("lutgemm_p2p_gemv_allgather", _I, [_P, ctypes.POINTER(lutgemm_weight), _P, _P, _SZ, _P, ctypes.POINTER(_P), _P]),
+    ("lutgemm_p2p_destroy", _I, [_P]),
     ("lutgemm_quantize_rtn", _I, [_P, _I, _I, _I, _I, _P, _P, _P, _P]),
     ("lutgemm_quantize_bcq", _I, [_P, _I, _I, _I, _I, _I, _P, _P, _P]),
     ("lutgemm_tp_unique_id", _I, [_P]),
@@ -306,3 +310,38 @@ def lutgemm_quantize_bcq(W: torch.Tensor, q: int, g: int, iters: int = 0, stream
     _check("lutgemm_quantize_bcq", lib.lutgemm_quantize_bcq(W.data_ptr(), m, n, q, g, iters, planes.data_ptr(),
                                                             alpha.data_ptr(), _stream(stream)))
     return planes, alpha
+
+
+class P2PGroup:
+    """Fused GEMV + rows all-gather over peer memory (lutgemm_p2p_*).
+    The 256-byte IPC records travel over the caller's torch.distributed group
+    (plumbing only; gloo or nccl); one process per GPU (or, for testing, per
+    process on one GPU)."""
+
+    def __init__(self, rank: int, world: int, out_elems: int, group=None):
+        import torch.distributed as dist
+        rec = (ctypes.c_uint8 * 256)()
+        h = _P()
+        _check("lutgemm_p2p_create", lib.lutgemm_p2p_create(rank, world, 2 * out_elems, ctypes.byref(h),
+                                                            ctypes.cast(rec, _P)))
+        self.handle, self.rank, self.world = h, rank, world
+        if world > 1:
+            recs = [None] * world
+            dist.all_gather_object(recs, bytes(rec), group=group)
+        else:
+            recs = [bytes(rec)]
+        allrec = (ctypes.c_uint8 * (256 * world)).from_buffer_copy(b"".join(recs))
+        _check("lutgemm_p2p_connect", lib.lutgemm_p2p_connect(self.handle, ctypes.cast(allrec, _P)))
+
+    def gemv_allgather(self, shard: PackedBCQ, x: torch.Tensor, ws: torch.Tensor, y: torch.Tensor | None = None,
+                       stream=None) -> torch.Tensor | None:
+        """Run one fused call; if y (CUDA fp16 [world * m_shard]) is given, the gathered result is copied there."""
+        _check("lutgemm_p2p_gemv_allgather",
+               lib.lutgemm_p2p_gemv_allgather(self.handle, ctypes.byref(shard.struct), x.data_ptr(), ws.data_ptr(),
+                                              ws.numel(), _stream(stream), None, _ptr(y)))
+        return y
+
+    def close(self):
+        if self.handle:
+            _check("lutgemm_p2p_destroy", lib.lutgemm_p2p_destroy(self.handle))
+            self.handle = None

@@ -46,12 +46,12 @@ def test_abi_version_and_sizes():
     # row-wise g > 1024: the group's scales repeat in each of the S slices; regions 256-B padded
     assert L.lutgemm_packed_bytes(8, 2048, 3, 2048, False) == 2 * (2 * 1536 + 256)
     # workspace: 2 x 256 u32 group counters + S*b*m4 fp32 split-K partials (256-B rounded)
-    assert L.lutgemm_workspace_bytes(49152, 12288, 1) == 2048 + 12 * 49152 * 4
+    assert L.lutgemm_workspace_bytes(49152, 12288, 1) == 2304 + 12 * 49152 * 4
     # b <= 4: sub-slice partials of the GEMV-structured kernel, [V S][b_pad][m4] fp32 (V = 4 for b = 3, 4)
-    assert L.lutgemm_workspace_bytes(49152, 12288, 4) == 2048 + 4 * 12 * 4 * 49152 * 4
-    assert L.lutgemm_workspace_bytes(5, 1056, 3) == 2048 + (4 * 2 * 4 * 8 * 4 + 255) // 256 * 256
-    assert L.lutgemm_workspace_bytes(49152, 12288, 2) == 2048 + 2 * 12 * 2 * 49152 * 4
-    assert L.lutgemm_workspace_bytes(49152, 12288, 8) == 2048 + 12 * 8 * 49152 * 4
+    assert L.lutgemm_workspace_bytes(49152, 12288, 4) == 2304 + 4 * 12 * 4 * 49152 * 4
+    assert L.lutgemm_workspace_bytes(5, 1056, 3) == 2304 + (4 * 2 * 4 * 8 * 4 + 255) // 256 * 256
+    assert L.lutgemm_workspace_bytes(49152, 12288, 2) == 2304 + 2 * 12 * 2 * 49152 * 4
+    assert L.lutgemm_workspace_bytes(49152, 12288, 8) == 2304 + 12 * 8 * 49152 * 4
 
 
 @pytest.mark.parametrize("m,n,q,g", [(0, 64, 3, 32), (8, 48, 3, 48), (8, 64, 0, 32), (8, 64, 9, 32),

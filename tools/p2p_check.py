@@ -1,0 +1,85 @@
+"""Fused GEMV + rows all-gather over peer memory (lutgemm_p2p_*), checked against
+the plain GEMV of the full (unsharded) layer: every rank's gathered output must be
+bitwise equal to the 1-GPU rows (same fixed-order reduction per row).
+
+    torchrun --nproc-per-node P tools/p2p_check.py [--same-device] [--rounds 5]
+
+--same-device puts every rank on cuda:0 (CUDA IPC works between processes on one
+GPU; the handles travel over gloo) -- the single-GPU validation of the multi-rank
+protocol.  Exits non-zero on a mismatch.
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2206_09557_b200 as L  # noqa: E402
+from workloads import gen_bcq, gen_x  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--same-device", action="store_true")
+    ap.add_argument("--rounds", type=int, default=5)
+    ap.add_argument("--m", type=int, default=8192)
+    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--timing", action="store_true")
+    a = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device("cuda", 0 if a.same_device else local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("gloo")
+    m, n, q, g = a.m, a.n, 3, 128
+    ms = m // world
+    d = gen_bcq(11, m, n, q, g)
+    planes = torch.from_numpy(d["planes"].view(np.int32)).to(dev)
+    alpha = torch.from_numpy(d["alpha"]).to(dev)
+    full = L.lutgemm_pack_bcq(planes, alpha, None, n, g)
+    shard = L.lutgemm_pack_bcq(planes[:, rank * ms:(rank + 1) * ms].contiguous(),
+                               alpha[rank * ms:(rank + 1) * ms].contiguous(), None, n, g)
+    grp = L.P2PGroup(rank, world, m)
+    ws = L.make_workspace(L.lutgemm_workspace_bytes(ms, n, 1), dev)
+    wsf = L.make_workspace(L.lutgemm_workspace_bytes(m, n, 1), dev)
+    ok = True
+    for r in range(a.rounds):
+        x = torch.from_numpy(gen_x(100 + r, 1, n)[0]).to(dev)
+        ref = L.lutgemm_gemv(full, x, None, wsf)
+        y = torch.empty(m, dtype=torch.float16, device=dev)
+        grp.gemv_allgather(shard, x, ws, y)
+        torch.cuda.synchronize()
+        same = torch.equal(y.view(torch.int16), ref.view(torch.int16))
+        ok &= bool(same)
+        print(f"rank {rank} round {r}: gathered == 1-GPU rows bitwise: {same}", flush=True)
+    if a.timing:  # fused call (GEMV + P2P all-gather + wait) vs the plain shard GEMV, events, eager
+        x = torch.from_numpy(gen_x(7, 1, n)[0]).to(dev)
+        yl = torch.empty(ms, dtype=torch.float16, device=dev)
+        for fn, name in ((lambda: grp.gemv_allgather(shard, x, ws), "fused gemv+allgather"),
+                         (lambda: L.lutgemm_gemv(shard, x, yl, ws), "shard gemv only")):
+            for _ in range(20):
+                fn()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(200):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            print(f"rank {rank} {name}: {e0.elapsed_time(e1) / 200 * 1e3:.2f} us/call", flush=True)
+    if world > 1:
+        dist.barrier()
+    grp.close()
+    if world > 1:
+        dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()
