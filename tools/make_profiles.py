@@ -203,7 +203,8 @@ def main(tag, rnd="01"):
         sl = [f"# Round {int(rnd)} -- compute-sanitizer over every kernel path (SURVEY 4, tier T4)", "",
               "Command: `bash tools/sanitize.sh` (runs `tools/sanitize_case.py` under each tool: GEMV fused and "
               "non-fused with one and many reducers, n and m tails, batched V=2 and V=4, q up to 6, fp32 output, "
-              "compact uniform format, the RTN / greedy / alternating quantizers; every result is checked against "
+              "compact uniform format, the RTN / greedy / alternating quantizers, the fused P2P all-gather at world 1; "
+              "every result is checked against "
               "the oracle).", "", "| tool | result | oracle checks passed |", "|---|---|---|"]
         for t, f in san.items():
             txt = open(f).read()

@@ -57,6 +57,21 @@ def main():
         rp, ra = Q.quantize_bcq_greedy(W, 3, 128) if iters == 0 else Q.quantize_bcq_alternating(W, 3, 128, iters)
         assert np.array_equal(p.cpu().numpy().view(np.uint32), rp) and np.array_equal(a.cpu().numpy(), ra)
         print(f"ok quantize_bcq iters={iters}", flush=True)
+    # fused rows all-gather over peer memory (NEXT-1), world 1
+    m, n = 6000, 4096
+    d = gen_bcq(9, m, n, 3, 128)
+    w = L.lutgemm_pack_bcq(dev(d["planes"].view(np.int32)), dev(d["alpha"]), None, n, 128)
+    grp = L.P2PGroup(0, 1, m)
+    ws = L.make_workspace(L.lutgemm_workspace_bytes(m, n, 1), "cuda")
+    for r in range(3):
+        x = dev(gen_x(r, 1, n)[0])
+        y = torch.empty(m, dtype=torch.float16, device="cuda")
+        grp.gemv_allgather(w, x, ws, y)
+        ref = L.lutgemm_gemv(w, x)
+        torch.cuda.synchronize()
+        assert torch.equal(y.view(torch.int16), ref.view(torch.int16))
+    grp.close()
+    print("ok p2p world 1", flush=True)
     torch.cuda.synchronize()
     print("sanitize cases done")
 
