@@ -61,8 +61,16 @@ def main():
     if a.timing:  # fused call (GEMV + P2P all-gather + wait) vs the plain shard GEMV, events, eager
         x = torch.from_numpy(gen_x(7, 1, n)[0]).to(dev)
         yl = torch.empty(ms, dtype=torch.float16, device=dev)
-        for fn, name in ((lambda: grp.gemv_allgather(shard, x, ws), "fused gemv+allgather"),
-                         (lambda: L.lutgemm_gemv(shard, x, yl, ws), "shard gemv only")):
+        fns = [(lambda: grp.gemv_allgather(shard, x, ws), "fused gemv+allgather (P2P epilogue)"),
+               (lambda: L.lutgemm_gemv(shard, x, yl, ws), "shard gemv only")]
+        if world == 1:  # the NCCL baseline at world 1: GEMV + ncclAllGather (lutgemm_tp_linear)
+            dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29599", world_size=1, rank=0,
+                                    device_id=dev)
+            comm = L.TPComm(0, 1, device=dev)
+            tws = L.make_workspace(comm.workspace_bytes(L.TP_ROWS_ALLGATHER, ms, n, 1), dev)
+            yg = torch.empty(m, dtype=torch.float16, device=dev)
+            fns.append((lambda: comm.linear(L.TP_ROWS_ALLGATHER, shard, x, yg, tws), "gemv + ncclAllGather"))
+        for fn, name in fns:
             for _ in range(20):
                 fn()
             torch.cuda.synchronize()
@@ -76,7 +84,7 @@ def main():
     if world > 1:
         dist.barrier()
     grp.close()
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
     sys.exit(0 if ok else 1)
 
