@@ -38,7 +38,7 @@ def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
-@pytest.mark.parametrize("b", [1, 3])
+@pytest.mark.parametrize("b", [1, 2, 3, 8])
 def test_tp_world1_modes(comm, b):
     import paper_2206_09557_b200 as L
     m, n, q, g = 1024, 2048, 3, 128
