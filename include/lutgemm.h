@@ -254,9 +254,10 @@ int lutgemm_tp_nranks(const lutgemm_tp* tp);
  * The tensor-parallel GEMV of ROWS_ALLGATHER with the collective fused into the
  * GEMV's epilogue: the reducer CTAs of rank r store each finished row of its
  * shard straight into every rank's output buffer over NVLink / NVSwitch (CUDA
- * IPC mappings), the grid's last reducer signals every rank at system scope,
- * and a one-thread wait kernel on the stream acquires until the rank has all P
- * signals of the round.  No NCCL call; one process per GPU.
+ * IPC mappings), the grid's last reducer signals every rank at system scope
+ * and keeps the grid open until the rank holds all P signals of the round, so
+ * the kernel's completion means "gathered output ready".  No NCCL call; one
+ * process per GPU.
  *
  * Each rank owns two output buffers (double buffer) and a signal counter.  The
  * output of a call stays valid until the call after next (flow control: a rank

@@ -510,7 +510,6 @@ inline cudaError_t launch(K kernel, int grid, const KParams& p, cudaStream_t st,
 
 // per-kernel-family launchers (dispatch on q and the scale format ZM)
 cudaError_t launch_gemv(const KParams& p, int grid, cudaStream_t st);
-cudaError_t launch_p2p_wait(const unsigned* sig, unsigned target, cudaStream_t st);
 cudaError_t launch_reduce(const KParams& p, cudaStream_t st);
 cudaError_t launch_batched(const KParams& p, int grid, cudaStream_t st);
 cudaError_t launch_reduce_batched(const KParams& p, cudaStream_t st);

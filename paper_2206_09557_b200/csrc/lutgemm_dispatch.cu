@@ -95,7 +95,7 @@ static bool fusable(int S, int units, int sms) {
 
 static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint16_t* x, int b, uint16_t* y, float* yf,
                                   void* ws, cudaStream_t st, __half* const* peer_y, unsigned* const* peer_sig,
-                                  int npeers, int yoff);
+                                  int npeers, int yoff, int self = 0, unsigned target = 0);
 
 cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, int b, uint16_t* y, float* yf,
                         void* ws, cudaStream_t st) {
@@ -103,17 +103,19 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
 }
 
 cudaError_t run_gemv_p2p(const Shape& sh, const void* data, const uint16_t* x, void* ws, __half* const* peer_y,
-                         unsigned* const* peer_sig, int npeers, int yoff, cudaStream_t st) {
-  if (npeers < 1 || npeers > 8) return cudaErrorInvalidValue;
-  return run_product_ex(sh, data, x, 1, nullptr, nullptr, ws, st, peer_y, peer_sig, npeers, yoff);
+                         unsigned* const* peer_sig, int npeers, int yoff, int self, unsigned target, cudaStream_t st) {
+  if (npeers < 1 || npeers > 8 || self < 0 || self >= npeers) return cudaErrorInvalidValue;
+  return run_product_ex(sh, data, x, 1, nullptr, nullptr, ws, st, peer_y, peer_sig, npeers, yoff, self, target);
 }
 
 static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint16_t* x, int b, uint16_t* y, float* yf,
                                   void* ws, cudaStream_t st, __half* const* peer_y, unsigned* const* peer_sig,
-                                  int npeers, int yoff) {
+                                  int npeers, int yoff, int self, unsigned target) {
   KParams p;
   p.npeers = npeers;
   p.yoff = yoff;
+  p.p2p_self = self;
+  p.p2p_target = target;
   for (int i = 0; i < 8; ++i) {
     p.peer_y[i] = i < npeers ? peer_y[i] : nullptr;
     p.peer_sig[i] = i < npeers ? peer_sig[i] : nullptr;

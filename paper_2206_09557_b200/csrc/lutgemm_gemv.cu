@@ -253,6 +253,11 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
         *done = 0u;
         fence_sc_sys();
         for (int pr = 0; pr < p.npeers; ++pr) red_release_sys_add_u32(p.peer_sig[pr], 1u);
+        // ... and holds the grid open until every rank's rows of this round have
+        // arrived here: the kernel's completion then means "gathered output ready"
+        if (p.p2p_target) {
+          while (ld_acquire_sys_u32(p.peer_sig[p.p2p_self]) < p.p2p_target) __nanosleep(64);
+        }
       }
     }
     if (trace) trace[6] = globaltimer_ns();  // reduction share done
@@ -314,20 +319,6 @@ struct GemvLaunch {
 
 cudaError_t launch_gemv(const KParams& p, int grid, cudaStream_t st) { return dispatch_qz<GemvLaunch>(p, grid, st); }
 
-// Fused rows all-gather, consumer side: wait until this rank's signal counter
-// reaches `target` (P signals per round), acquire at system scope.
-// (A programmatic-dependent launch of this kernel, overlapping the GEMV's tail,
-// measured slower: 59.4 vs 57.4 us per fc1 call at world 1.)
-__global__ void p2p_wait_kernel(const unsigned* sig, unsigned target) {
-  if (threadIdx.x == 0) {
-    while (ld_acquire_sys_u32(sig) < target) __nanosleep(64);
-  }
-}
-
-cudaError_t launch_p2p_wait(const unsigned* sig, unsigned target, cudaStream_t st) {
-  p2p_wait_kernel<<<1, 32, 0, st>>>(sig, target);
-  return cudaGetLastError();
-}
 
 cudaError_t launch_reduce(const KParams& p, cudaStream_t st) {
   g_launches.fetch_add(1, std::memory_order_relaxed);

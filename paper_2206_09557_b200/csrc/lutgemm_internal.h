@@ -31,6 +31,8 @@ struct KParams {
   unsigned* peer_sig[8];
   int npeers;        // 0: plain output
   int yoff;
+  int p2p_self;      // this rank's index in peer_sig
+  unsigned p2p_target;  // nonzero: the grid's last reducer waits until peer_sig[p2p_self] >= target
   int s2;            // b <= 4 GEMV-structured kernel: number of sub-slices (0: not used)
   long long items;
   unsigned long long* trace;  // optional per-CTA timeline (kTraceSlots u64 per CTA), or null
@@ -55,10 +57,10 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
 
 // NEXT-1: b = 1 product whose fused reduction stores the rows into every rank's
 // output (peer_y[pr] + yoff) and signals every rank (peer_sig[pr]); requires the
-// fused GEMV mode (returns cudaErrorNotSupported otherwise).  Then the wait.
+// fused GEMV mode (returns cudaErrorNotSupported otherwise); the grid's last
+// reducer then waits until peer_sig[self] >= target (the round's P signals).
 cudaError_t run_gemv_p2p(const Shape& sh, const void* data, const uint16_t* x, void* ws, __half* const* peer_y,
-                         unsigned* const* peer_sig, int npeers, int yoff, cudaStream_t st);
-cudaError_t launch_p2p_wait(const unsigned* sig, unsigned target, cudaStream_t st);
+                         unsigned* const* peer_sig, int npeers, int yoff, int self, unsigned target, cudaStream_t st);
 
 cudaError_t run_pack_bcq(const Shape& sh, const uint32_t* planes, const uint16_t* alpha, const uint16_t* offset,
                          void* dst, cudaStream_t st);

@@ -9,8 +9,9 @@
 // torch.distributed).  A call runs the fused GEMV whose reducer CTAs store each
 // finished row of this rank's shard straight into buffer (round & 1) of every
 // rank (NVLink / NVSwitch P2P stores), then the grid's last reducer signals
-// every rank (red.release.sys); a one-thread wait kernel on the stream acquires
-// until this rank has received P signals for the round.  Flow control: a rank
+// every rank (red.release.sys) and then holds the grid open until this rank has
+// received the round's P signals (ld.acquire.sys), so the kernel's completion
+// means "gathered output ready" for whatever the stream runs next.  Flow control: a rank
 // writes buffer (k+2) & 1 only after its wait for round k+1, which needs every
 // peer's round-(k+1) signal, sent after that peer's stream ran everything before
 // its round-(k+1) call -- including its consumers of round k.  Contract: the
@@ -134,13 +135,14 @@ lutgemm_status lutgemm_p2p_gemv_allgather(lutgemm_p2p* g, const lutgemm_weight* 
   const int parity = (int)(g->round & 1);
   __half* peer_y[8];
   for (int pr = 0; pr < g->nranks; ++pr) peer_y[pr] = static_cast<__half*>(g->peer_out[parity][pr]);
-  cudaError_t e = lg::run_gemv_p2p(sh, shard->data, x, ws, peer_y, g->peer_sig, g->nranks, g->rank * shard->m, st);
+  // the grid's last reducer waits for the round's P signals itself (no wait kernel)
+  const unsigned target = (unsigned)((g->round + 1) * g->nranks);
+  cudaError_t e = lg::run_gemv_p2p(sh, shard->data, x, ws, peer_y, g->peer_sig, g->nranks, g->rank * shard->m,
+                                   g->rank, target, st);
   if (e == cudaErrorNotSupported)
     return lutgemm_internal_fail(LUTGEMM_ERR_UNSUPPORTED, "shard shape does not run the fused GEMV mode");
   if (e != cudaSuccess) return cuda_fail(e, "fused GEMV launch");
   g->round += 1;
-  e = lg::launch_p2p_wait(g->sig, (unsigned)(g->round * g->nranks), st);
-  if (e != cudaSuccess) return cuda_fail(e, "p2p wait launch");
   if (y_copy) {
     e = cudaMemcpyAsync(y_copy, g->out[parity], m_total * 2, cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return cuda_fail(e, "output copy");
