@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     __syncthreads();
     // fused all-gather: the CTA's peer stores (ordered before thread 0 by the
     // barrier) are made visible at system scope before any count below
-    if (p.npeers > 0 && tid == 0) fence_sc_sys();
+    if (p.npeers > 0 && tid == 0) fence_acq_rel_sys();
     if (tid == 0 && atomicAdd(depart, 1u) == (unsigned)R - 1) {  // the last reducer resets the pair
       *arrive = 0u;
       *depart = 0u;
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
       unsigned* done = p.counters + 2 * kFusedMaxJ;
       if (atom_add_acq_rel_u32(done, 1u) == (unsigned)(J * R) - 1) {
         *done = 0u;
-        fence_sc_sys();
+        fence_acq_rel_sys();
         for (int pr = 0; pr < p.npeers; ++pr) red_release_sys_add_u32(p.peer_sig[pr], 1u);
         // ... and holds the grid open until every rank's rows of this round have
         // arrived here: the kernel's completion then means "gathered output ready"
