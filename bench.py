@@ -279,10 +279,13 @@ def run_gpu(args, cfg) -> None:
     stream = torch.cuda.current_stream()
     if world > 1:
         tws = L.make_workspace(comm.workspace_bytes(L.TP_ROWS_ALLGATHER, m, n, 1), dev)
+        p2p = L.P2PGroup(rank, world, m * world) if args.tp_impl == "p2p" else None
 
     def step(i):
         w = ws_list[i % ncopies]
-        if world > 1:
+        if world > 1 and p2p is not None:  # fused all-gather in the GEMV epilogue (NEXT-1)
+            p2p.gemv_allgather(w, x, ws)
+        elif world > 1:
             comm.linear(L.TP_ROWS_ALLGATHER, w, x, y, tws)
         else:
             L.lutgemm_gemv(w, x, y, ws)
@@ -410,7 +413,8 @@ def run_gpu(args, cfg) -> None:
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded uniform random bit-planes, alpha ~ 0.87*2^-i*U(.75,1.25)/sqrt(n), x ~ N(0,1) fp16)",
             "config": {"workload": cfg["name"] + " (OPT-175B FFN-1: in 12288 -> out 49152)", "m": m, "n": n, "q": q,
-                       "g": g, "b": 1, "parallelism": f"tp{world} rows+allgather" if world > 1 else "single GPU",
+                       "g": g, "b": 1,
+                       "parallelism": (f"tp{world} rows+allgather ({args.tp_impl})" if world > 1 else "single GPU"),
                        "l2": f"{ncopies} rotating weight copies = {ncopies * B / 1e6:.0f} MB > 3x L2 ({l2 / 1e6:.0f} MB)",
                        "bytes_alg_per_gemv": B},
             "us_per_gemv": round(ms_per_step * 1e3, 3),
@@ -435,6 +439,8 @@ def run_gpu(args, cfg) -> None:
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        if p2p is not None:
+            p2p.close()
         comm.close()
         torch.distributed.destroy_process_group()
 
@@ -451,6 +457,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
+    ap.add_argument("--tp-impl", default="nccl", choices=["nccl", "p2p"],
+                    help="N > 1: GEMV + ncclAllGather, or the all-gather fused into the GEMV epilogue over peer memory")
     args = ap.parse_args()
     from workloads import CONFIGS
     cfg = dict(CONFIGS[args.config], name=args.config)
