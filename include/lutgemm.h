@@ -282,6 +282,15 @@ lutgemm_status lutgemm_p2p_connect(lutgemm_p2p* g, const uint8_t* records);
  * quads for the J CTAs per slice, or more slices than SMs). */
 lutgemm_status lutgemm_p2p_gemv_allgather(lutgemm_p2p* g, const lutgemm_weight* shard, const uint16_t* x, void* ws,
                                           size_t ws_bytes, void* stream, uint16_t** y_full, uint16_t* y_copy);
+/* Column split (Megatron's second linear): y [m] (fp16, device, caller-owned)
+ * = sum over ranks of (shard_r [m][n/P]) x_r, x_r = this rank's slice of x.
+ * The fused GEMV's reducers store this rank's fp32 partial rows into slot
+ * `rank` of every rank's current buffer (P2P), signal as above, and a small
+ * kernel then sums the P slots of this rank in rank order (deterministic,
+ * within tolerance of the 1-GPU result) and rounds to fp16.  Buffers must hold
+ * P * m fp32 (out_bytes >= 4 P m). */
+lutgemm_status lutgemm_p2p_gemv_allreduce(lutgemm_p2p* g, const lutgemm_weight* shard, const uint16_t* x, void* ws,
+                                          size_t ws_bytes, void* stream, uint16_t* y);
 /* Synchronises the device, closes the peer mappings and frees the buffers. */
 lutgemm_status lutgemm_p2p_destroy(lutgemm_p2p* g);
 

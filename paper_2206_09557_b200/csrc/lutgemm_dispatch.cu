@@ -95,7 +95,7 @@ static bool fusable(int S, int units, int sms) {
 
 static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint16_t* x, int b, uint16_t* y, float* yf,
                                   void* ws, cudaStream_t st, __half* const* peer_y, unsigned* const* peer_sig,
-                                  int npeers, int yoff, int self = 0, unsigned target = 0);
+                                  int npeers, int yoff, int self = 0, unsigned target = 0, int f32 = 0);
 
 cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, int b, uint16_t* y, float* yf,
                         void* ws, cudaStream_t st) {
@@ -103,15 +103,17 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
 }
 
 cudaError_t run_gemv_p2p(const Shape& sh, const void* data, const uint16_t* x, void* ws, __half* const* peer_y,
-                         unsigned* const* peer_sig, int npeers, int yoff, int self, unsigned target, cudaStream_t st) {
+                         unsigned* const* peer_sig, int npeers, int yoff, int self, unsigned target, int f32,
+                         cudaStream_t st) {
   if (npeers < 1 || npeers > 8 || self < 0 || self >= npeers) return cudaErrorInvalidValue;
-  return run_product_ex(sh, data, x, 1, nullptr, nullptr, ws, st, peer_y, peer_sig, npeers, yoff, self, target);
+  return run_product_ex(sh, data, x, 1, nullptr, nullptr, ws, st, peer_y, peer_sig, npeers, yoff, self, target, f32);
 }
 
 static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint16_t* x, int b, uint16_t* y, float* yf,
                                   void* ws, cudaStream_t st, __half* const* peer_y, unsigned* const* peer_sig,
-                                  int npeers, int yoff, int self, unsigned target) {
+                                  int npeers, int yoff, int self, unsigned target, int f32) {
   KParams p;
+  p.p2p_f32 = f32;
   p.npeers = npeers;
   p.yoff = yoff;
   p.p2p_self = self;

@@ -228,7 +228,9 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
         for (int kk = 0; kk < 16; ++kk)
           if (ss0 + kk < sh.S) v += t[kk];
       }
-      if (p.npeers > 0) {  // fused rows all-gather (NEXT-1): the row goes to every rank's output over NVLink
+      if (p.npeers > 0 && p.p2p_f32) {  // fused all-reduce: fp32 partial row into slot `rank` of every rank
+        for (int pr = 0; pr < p.npeers; ++pr) reinterpret_cast<float*>(p.peer_y[pr])[p.yoff + r] = v;
+      } else if (p.npeers > 0) {  // fused rows all-gather (NEXT-1): the row goes to every rank's output over NVLink
         const __half h = __float2half_rn(v);
         for (int pr = 0; pr < p.npeers; ++pr) p.peer_y[pr][p.yoff + r] = h;
       } else if (p.yf) {
@@ -319,7 +321,6 @@ struct GemvLaunch {
 
 cudaError_t launch_gemv(const KParams& p, int grid, cudaStream_t st) { return dispatch_qz<GemvLaunch>(p, grid, st); }
 
-
 cudaError_t launch_reduce(const KParams& p, cudaStream_t st) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   static bool attr_set = false;
@@ -338,6 +339,36 @@ cudaError_t launch_reduce(const KParams& p, cudaStream_t st) {
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, lut_reduce_kernel, (const float*)p.partial, p.sh.S, p.b, p.sh.m, p.sh.m4, p.y,
                             p.yf);
+}
+
+// Fused all-reduce, local step: y[r] = sum over ranks pr = 0..P-1 (fixed order,
+// deterministic) of slot[pr][r], fp16 round-to-nearest-even.  Launched with PDL
+// behind the fused GEMV (which triggers its dependents early), so its CTAs are
+// resident and waiting when the GEMV's last reducer has seen the round's signals.
+__global__ void __launch_bounds__(256) p2p_sum_kernel(const float* __restrict__ slots, int P, int m,
+                                                      __half* __restrict__ y) {
+  pdl_wait();
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  float v = __ldcg(slots + r);
+  for (int pr = 1; pr < P; ++pr) v += __ldcg(slots + (size_t)pr * m + r);
+  y[r] = __float2half_rn(v);
+}
+
+cudaError_t launch_p2p_sum(const float* slots, int P, int m, uint16_t* y, cudaStream_t st) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  static bool attr_set = false;
+  if (!attr_set) {  // same carveout as the GEMV: no L1/smem reconfiguration, co-resident while waiting
+    cudaFuncSetAttribute(p2p_sum_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((m + 255) / 256);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cfg.attrs = const_cast<cudaLaunchAttribute*>(pdl_attr());
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, p2p_sum_kernel, slots, P, m, reinterpret_cast<__half*>(y));
 }
 
 }  // namespace lg

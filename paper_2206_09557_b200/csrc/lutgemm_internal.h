@@ -32,6 +32,7 @@ struct KParams {
   int npeers;        // 0: plain output
   int yoff;
   int p2p_self;      // this rank's index in peer_sig
+  int p2p_f32;       // 1: store fp32 partial rows (fused column-split all-reduce) instead of fp16 rows
   unsigned p2p_target;  // nonzero: the grid's last reducer waits until peer_sig[p2p_self] >= target
   int s2;            // b <= 4 GEMV-structured kernel: number of sub-slices (0: not used)
   long long items;
@@ -60,7 +61,9 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
 // fused GEMV mode (returns cudaErrorNotSupported otherwise); the grid's last
 // reducer then waits until peer_sig[self] >= target (the round's P signals).
 cudaError_t run_gemv_p2p(const Shape& sh, const void* data, const uint16_t* x, void* ws, __half* const* peer_y,
-                         unsigned* const* peer_sig, int npeers, int yoff, int self, unsigned target, cudaStream_t st);
+                         unsigned* const* peer_sig, int npeers, int yoff, int self, unsigned target, int f32,
+                         cudaStream_t st);
+cudaError_t launch_p2p_sum(const float* slots, int P, int m, uint16_t* y, cudaStream_t st);
 
 cudaError_t run_pack_bcq(const Shape& sh, const uint32_t* planes, const uint16_t* alpha, const uint16_t* offset,
                          void* dst, cudaStream_t st);

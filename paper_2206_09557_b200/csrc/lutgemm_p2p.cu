@@ -138,7 +138,7 @@ lutgemm_status lutgemm_p2p_gemv_allgather(lutgemm_p2p* g, const lutgemm_weight* 
   // the grid's last reducer waits for the round's P signals itself (no wait kernel)
   const unsigned target = (unsigned)((g->round + 1) * g->nranks);
   cudaError_t e = lg::run_gemv_p2p(sh, shard->data, x, ws, peer_y, g->peer_sig, g->nranks, g->rank * shard->m,
-                                   g->rank, target, st);
+                                   g->rank, target, 0, st);
   if (e == cudaErrorNotSupported)
     return lutgemm_internal_fail(LUTGEMM_ERR_UNSUPPORTED, "shard shape does not run the fused GEMV mode");
   if (e != cudaSuccess) return cuda_fail(e, "fused GEMV launch");
@@ -148,6 +148,37 @@ lutgemm_status lutgemm_p2p_gemv_allgather(lutgemm_p2p* g, const lutgemm_weight* 
     if (e != cudaSuccess) return cuda_fail(e, "output copy");
   }
   if (y_full) *y_full = static_cast<uint16_t*>(g->out[parity]);
+  return LUTGEMM_OK;
+}
+
+lutgemm_status lutgemm_p2p_gemv_allreduce(lutgemm_p2p* g, const lutgemm_weight* shard, const uint16_t* x, void* ws,
+                                          size_t ws_bytes, void* stream, uint16_t* y) {
+  if (!g || !g->connected || !shard || !shard->data || !x || !ws || !y)
+    return lutgemm_internal_fail(LUTGEMM_ERR_INVALID_ARG, "NULL argument or group not connected");
+  const size_t m = (size_t)shard->m;
+  if ((size_t)g->nranks * m * 4 > g->out_bytes)
+    return lutgemm_internal_fail(LUTGEMM_ERR_INVALID_ARG, "buffers too small for nranks * m fp32 partial rows");
+  if (lutgemm_workspace_bytes(shard->m, shard->n, 1) > ws_bytes)
+    return lutgemm_internal_fail(LUTGEMM_ERR_WORKSPACE, "workspace too small");
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(ws) & 15) ||
+      (reinterpret_cast<uintptr_t>(shard->data) & 15) || (reinterpret_cast<uintptr_t>(y) & 1))
+    return lutgemm_internal_fail(LUTGEMM_ERR_MISALIGNED, "x, ws and the weight must be 16-byte aligned");
+  const lg::Shape sh = lg::make_shape(shard->m, shard->n, shard->q, shard->g, shard->has_offset,
+                                      shard->format == LUTGEMM_FMT_UNIFORM_COMPACT);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int parity = (int)(g->round & 1);
+  __half* peer_y[8];
+  for (int pr = 0; pr < g->nranks; ++pr) peer_y[pr] = static_cast<__half*>(g->peer_out[parity][pr]);
+  const unsigned target = (unsigned)((g->round + 1) * g->nranks);
+  // fp32 partial row r of this rank -> slot [rank][r] of every rank
+  cudaError_t e = lg::run_gemv_p2p(sh, shard->data, x, ws, peer_y, g->peer_sig, g->nranks,
+                                   (int)(g->rank * m), g->rank, target, 1, st);
+  if (e == cudaErrorNotSupported)
+    return lutgemm_internal_fail(LUTGEMM_ERR_UNSUPPORTED, "shard shape does not run the fused GEMV mode");
+  if (e != cudaSuccess) return cuda_fail(e, "fused GEMV launch");
+  g->round += 1;
+  e = lg::launch_p2p_sum(static_cast<const float*>(g->out[parity]), g->nranks, (int)m, y, st);
+  if (e != cudaSuccess) return cuda_fail(e, "p2p sum launch");
   return LUTGEMM_OK;
 }
 

@@ -65,6 +65,7 @@ SIGNATURES = [
     ("lutgemm_p2p_create", _I, [_I, _I, _SZ, ctypes.POINTER(_P), _P]),
     ("lutgemm_p2p_connect", _I, [_P, _P]),
     ("lutgemm_p2p_gemv_allgather", _I, [_P, ctypes.POINTER(lutgemm_weight), _P, _P, _SZ, _P, ctypes.POINTER(_P), _P]),
+    ("lutgemm_p2p_gemv_allreduce", _I, [_P, ctypes.POINTER(lutgemm_weight), _P, _P, _SZ, _P, _P]),
     ("lutgemm_p2p_destroy", _I, [_P]),
     ("lutgemm_quantize_rtn", _I, [_P, _I, _I, _I, _I, _P, _P, _P, _P]),
     ("lutgemm_quantize_bcq", _I, [_P, _I, _I, _I, _I, _I, _P, _P, _P]),
@@ -318,11 +319,12 @@ class P2PGroup:
     (plumbing only; gloo or nccl); one process per GPU (or, for testing, per
     process on one GPU)."""
 
-    def __init__(self, rank: int, world: int, out_elems: int, group=None):
+    def __init__(self, rank: int, world: int, out_elems: int, group=None, out_bytes: int | None = None):
         import torch.distributed as dist
         rec = (ctypes.c_uint8 * 256)()
         h = _P()
-        _check("lutgemm_p2p_create", lib.lutgemm_p2p_create(rank, world, 2 * out_elems, ctypes.byref(h),
+        nbytes = out_bytes if out_bytes is not None else 2 * out_elems
+        _check("lutgemm_p2p_create", lib.lutgemm_p2p_create(rank, world, nbytes, ctypes.byref(h),
                                                             ctypes.cast(rec, _P)))
         self.handle, self.rank, self.world = h, rank, world
         if world > 1:
@@ -339,6 +341,14 @@ class P2PGroup:
         _check("lutgemm_p2p_gemv_allgather",
                lib.lutgemm_p2p_gemv_allgather(self.handle, ctypes.byref(shard.struct), x.data_ptr(), ws.data_ptr(),
                                               ws.numel(), _stream(stream), None, _ptr(y)))
+        return y
+
+    def gemv_allreduce(self, shard: PackedBCQ, x_local: torch.Tensor, ws: torch.Tensor, y: torch.Tensor,
+                       stream=None) -> torch.Tensor:
+        """Column split: y [m] fp16 = sum over ranks of shard_r x_r (fused fp32 partial exchange)."""
+        _check("lutgemm_p2p_gemv_allreduce",
+               lib.lutgemm_p2p_gemv_allreduce(self.handle, ctypes.byref(shard.struct), x_local.data_ptr(),
+                                              ws.data_ptr(), ws.numel(), _stream(stream), y.data_ptr()))
         return y
 
     def close(self):

@@ -34,6 +34,24 @@ def test_p2p_world1_matches_gemv():
     grp.close()
 
 
+def test_p2p_allreduce_world1_matches_gemv():
+    import paper_2206_09557_b200 as L
+    m, n, q, g = 6000, 4096, 3, 128
+    d = gen_bcq(5, m, n, q, g)
+    w = L.lutgemm_pack_bcq(torch.from_numpy(d["planes"].view(np.int32)).cuda(), torch.from_numpy(d["alpha"]).cuda(),
+                           None, n, g)
+    grp = L.P2PGroup(0, 1, m, out_bytes=4 * m)
+    ws = L.make_workspace(L.lutgemm_workspace_bytes(m, n, 1), "cuda")
+    for r in range(5):
+        x = torch.from_numpy(gen_x(r, 1, n)[0]).cuda()
+        y = torch.empty(m, dtype=torch.float16, device="cuda")
+        grp.gemv_allreduce(w, x, ws, y)
+        ref = L.lutgemm_gemv(w, x)
+        torch.cuda.synchronize()
+        assert torch.equal(y.view(torch.int16), ref.view(torch.int16))  # one slot: the fp16 of the same fp32 row
+    grp.close()
+
+
 def test_p2p_rejects_unfused_shapes():
     import paper_2206_09557_b200 as L
     d = gen_bcq(4, 8, 1024, 3, 128)  # 2 row quads < J CTAs per slice: not the fused mode
@@ -56,3 +74,14 @@ def test_p2p_multi_process_same_gpu(nproc):
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert out.count("bitwise: True") == 4 * nproc and "bitwise: False" not in out
+
+
+@pytest.mark.parametrize("nproc", [2, 4])
+def test_p2p_allreduce_multi_process_same_gpu(nproc):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29550 + nproc),
+           os.path.join(ROOT, "tools", "p2p_check.py"), "--same-device", "--rounds", "4", "--mode", "cols"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert out.count(": PASS") == 4 * nproc and ": FAIL" not in out
