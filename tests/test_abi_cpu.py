@@ -82,3 +82,19 @@ def test_gemv_argument_validation_without_gpu():
     w.has_offset, w.data = 0, 4100
     st = lib.lutgemm_gemv(ctypes.byref(w), 4096, 8192, 16384, 1 << 20, None)
     assert st == 2 and b"weight data" in lib.lutgemm_last_error()
+
+
+def test_p2p_argument_validation_without_gpu():
+    """lutgemm_p2p_*: bad arguments are rejected before any CUDA call (status 1 = INVALID_ARG)."""
+    import paper_2206_09557_b200.lutgemm as B
+    lib = B.lib
+    rec = (ctypes.c_uint8 * 256)()
+    h = ctypes.c_void_p()
+    for rank, world in [(0, 0), (0, 9), (2, 2), (-1, 2)]:
+        assert lib.lutgemm_p2p_create(rank, world, 1024, ctypes.byref(h), rec) == 1
+    assert lib.lutgemm_p2p_create(0, 1, 0, ctypes.byref(h), rec) == 1   # out_bytes 0
+    assert lib.lutgemm_p2p_connect(None, rec) == 1
+    w = B.lutgemm_weight()
+    assert lib.lutgemm_p2p_gemv_allgather(None, ctypes.byref(w), None, None, 0, None, None, None) == 1
+    assert lib.lutgemm_p2p_gemv_allreduce(None, ctypes.byref(w), None, None, 0, None, None) == 1
+    assert lib.lutgemm_p2p_destroy(None) == 0

@@ -71,6 +71,15 @@ def main():
         torch.cuda.synchronize()
         assert torch.equal(y.view(torch.int16), ref.view(torch.int16))
     grp.close()
+    grp = L.P2PGroup(0, 1, m, out_bytes=4 * m)  # fused column all-reduce (fp32 slots + P-way sum)
+    for r in range(3):
+        x = dev(gen_x(r, 1, n)[0])
+        y = torch.empty(m, dtype=torch.float16, device="cuda")
+        grp.gemv_allreduce(w, x, ws, y)
+        ref = L.lutgemm_gemv(w, x)
+        torch.cuda.synchronize()
+        assert torch.equal(y.view(torch.int16), ref.view(torch.int16))
+    grp.close()
     print("ok p2p world 1", flush=True)
     torch.cuda.synchronize()
     print("sanitize cases done")
