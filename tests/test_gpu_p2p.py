@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 import torch
 
-from workloads import gen_bcq, gen_x
+from workloads import gen_bcq, gen_uniform, gen_x
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -49,6 +49,30 @@ def test_p2p_allreduce_world1_matches_gemv():
         ref = L.lutgemm_gemv(w, x)
         torch.cuda.synchronize()
         assert torch.equal(y.view(torch.int16), ref.view(torch.int16))  # one slot: the fp16 of the same fp32 row
+    grp.close()
+
+
+@pytest.mark.parametrize("compact", [False, True])
+@pytest.mark.parametrize("mode", ["allgather", "allreduce"])
+def test_p2p_world1_uniform_offset_formats(mode, compact):
+    """The epilogue stores under the offset (extended BCQ, App. C) and compact uniform weights."""
+    import paper_2206_09557_b200 as L
+    m, n, q, g = 4096, 8192, 4, 128
+    u = gen_uniform(6, m, n, q, g)
+    w = L.lutgemm_pack_uniform(torch.from_numpy(u["codes"]).cuda(), torch.from_numpy(u["scale"]).cuda(),
+                               torch.from_numpy(u["zero"]).cuda(), q, g, compact=compact)
+    grp = L.P2PGroup(0, 1, m, out_bytes=4 * m)
+    ws = L.make_workspace(L.lutgemm_workspace_bytes(m, n, 1), "cuda")
+    for r in range(3):
+        x = torch.from_numpy(gen_x(20 + r, 1, n)[0]).cuda()
+        y = torch.empty(m, dtype=torch.float16, device="cuda")
+        if mode == "allgather":
+            grp.gemv_allgather(w, x, ws, y)
+        else:
+            grp.gemv_allreduce(w, x, ws, y)
+        ref = L.lutgemm_gemv(w, x)
+        torch.cuda.synchronize()
+        assert torch.equal(y.view(torch.int16), ref.view(torch.int16))
     grp.close()
 
 
