@@ -112,6 +112,11 @@ typedef struct {
 /* Library ABI version (LUTGEMM_ABI_VERSION). */
 int lutgemm_abi_version(void);
 
+/* sha256 prefix (24 hex digits) of the sources and compile flags this library
+ * was built from (paper_2206_09557_b200/_build.py); the Python binding refuses
+ * to load a library whose hash differs from the tree it sits in. */
+const char* lutgemm_source_hash(void);
+
 /* Thread-local text for the last non-OK status returned on this thread. */
 const char* lutgemm_last_error(void);
 

@@ -1,6 +1,6 @@
 """Build liblutgemm.so in-tree with nvcc for sm_100a (no torch needed).
 
-    python -m paper_2206_09557_b200._build [--verbose]
+    python paper_2206_09557_b200/_build.py [--verbose] [--force]
 
 Compiles every csrc/*.cu to an object in parallel, then links one shared
 library against the CUDA runtime and the NCCL that PyTorch ships (pip
@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import concurrent.futures as cf
 import glob
+import hashlib
 import os
 import subprocess
 import sys
@@ -46,17 +47,51 @@ def nvcc() -> str:
     return "nvcc"
 
 
+FLAGS = ["-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+         "--expt-relaxed-constexpr"]
+HASH_MARK = b"LUTGEMM_SRC_HASH:"
+
+
+def source_files() -> list[str]:
+    srcs = glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
+        glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(INCLUDE, "lutgemm.h")]
+    return sorted(srcs)
+
+
+def source_hash() -> str:
+    """sha256 (first 24 hex digits) over every source file's name and bytes and the compile flags:
+    embedded in the library (lutgemm_source_hash) so a loaded .so provably matches the tree."""
+    h = hashlib.sha256()
+    for p in source_files():
+        h.update(os.path.basename(p).encode() + b"\0")
+        with open(p, "rb") as f:
+            h.update(f.read())
+        h.update(b"\0")
+    h.update(" ".join(FLAGS).encode())
+    return h.hexdigest()[:24]
+
+
+def library_hash(path: str = LIB) -> str | None:
+    """The source hash embedded in a built library (None if absent or unmarked)."""
+    if not os.path.exists(path):
+        return None
+    with open(path, "rb") as f:
+        data = f.read()
+    i = data.find(HASH_MARK)
+    if i < 0:
+        return None
+    return data[i + len(HASH_MARK):i + len(HASH_MARK) + 24].decode(errors="replace")
+
+
 def build(verbose: bool = False, force: bool = False) -> str:
+    """Compile unless the library already embeds the hash of the current sources (force: always)."""
     os.makedirs(BUILD, exist_ok=True)
     inc, lib = nccl_dirs()
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
-    deps = srcs + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + \
-        [os.path.join(INCLUDE, "lutgemm.h")]
-    newest = max(os.path.getmtime(d) for d in deps)
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
+    want = source_hash()
+    if not force and library_hash() == want:
         return LIB
-    flags = ["-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-             "-I", INCLUDE, "-I", CSRC, "-I", inc, "--expt-relaxed-constexpr"]
+    flags = [*FLAGS, "-I", INCLUDE, "-I", CSRC, "-I", inc, f"-DLUTGEMM_SOURCE_HASH=\"{want}\""]
 
     def compile_one(src: str) -> tuple[str, str]:
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")

@@ -102,9 +102,17 @@ lutgemm_status product(const lutgemm_weight* w, const uint16_t* X, int b, uint16
 
 }  // namespace
 
+#ifndef LUTGEMM_SOURCE_HASH
+#define LUTGEMM_SOURCE_HASH "unhashed-build----------"
+#endif
+// marker + 24 hex digits: _build.py finds it in the binary to decide whether to recompile
+static const char kSourceHash[] = "LUTGEMM_SRC_HASH:" LUTGEMM_SOURCE_HASH;
+
 extern "C" {
 
 int lutgemm_abi_version(void) { return LUTGEMM_ABI_VERSION; }
+
+const char* lutgemm_source_hash(void) { return kSourceHash + 17; }
 
 const char* lutgemm_last_error(void) { return g_err; }
 

@@ -48,6 +48,7 @@ _I = ctypes.c_int
 SIGNATURES = [
     ("lutgemm_abi_version", _I, []),
     ("lutgemm_last_error", ctypes.c_char_p, []),
+    ("lutgemm_source_hash", ctypes.c_char_p, []),
     ("lutgemm_packed_bytes", _I, [_I, _I, _I, _I, _I, ctypes.POINTER(_SZ)]),
     ("lutgemm_packed_bytes_fmt", _I, [_I, _I, _I, _I, _I, _I, ctypes.POINTER(_SZ)]),
     ("lutgemm_pack_bcq", _I, [ctypes.POINTER(lutgemm_pack_src), ctypes.POINTER(lutgemm_weight), _P]),
@@ -85,9 +86,20 @@ def _load():
                           "there is no CPU fallback for the LUT-GEMM path")
     lib = ctypes.CDLL(LIB_PATH)
     for name, res, args in SIGNATURES:
-        fn = getattr(lib, name)
+        try:
+            fn = getattr(lib, name)
+        except AttributeError as e:
+            raise ImportError(f"{LIB_PATH} lacks {name} (stale build): rebuild with "
+                              "`python -c 'import __graft_entry__ as g; g.build()'`") from e
         fn.restype = res
         fn.argtypes = args
+    # the library must be the build of the sources next to it (no stale binary)
+    if os.path.isdir(os.path.join(_HERE, "csrc")):
+        from paper_2206_09557_b200._build import source_hash
+        have, want = lib.lutgemm_source_hash().decode(), source_hash()
+        if have != want:
+            raise ImportError(f"{LIB_PATH} was built from sources {have}, the tree has {want}: rebuild with "
+                              "`python -c 'import __graft_entry__ as g; g.build()'`")
     return lib
 
 

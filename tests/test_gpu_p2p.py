@@ -1,6 +1,7 @@
-"""Fused GEMV + rows all-gather over peer memory (lutgemm_p2p_*):
-world 1 in-process, and 2 / 4 processes sharing the one GPU through CUDA IPC
-(the handles travel over gloo) -- every rank's gathered output must equal the
+"""Fused GEMV + rows all-gather / column all-reduce over peer memory (SURVEY NEXT-1,
+lutgemm_p2p_*): world 1 in-process, and 2 / 4 processes sharing the one GPU through
+CUDA IPC (the handles travel over gloo).  Every result is checked against the fp64
+oracle at the north_star tolerances; in addition the gathered rows must equal the
 1-GPU rows bit for bit, over several rounds (both halves of the double buffer)."""
 import os
 import subprocess
@@ -10,6 +11,8 @@ import numpy as np
 import pytest
 import torch
 
+import oracle as O
+from tests._helpers import assert_parity
 from workloads import gen_bcq, gen_uniform, gen_x
 
 pytestmark = pytest.mark.gpu
@@ -30,6 +33,8 @@ def test_p2p_world1_matches_gemv():
         grp.gemv_allgather(w, x, ws, y)
         ref = L.lutgemm_gemv(w, x)
         torch.cuda.synchronize()
+        assert_parity(y.float().cpu().numpy(), O.bcq_gemv(d["planes"], d["alpha"], None, gen_x(r, 1, n), n, g),
+                      ("p2p rows", r))
         assert torch.equal(y.view(torch.int16), ref.view(torch.int16))
     grp.close()
 
@@ -48,6 +53,8 @@ def test_p2p_allreduce_world1_matches_gemv():
         grp.gemv_allreduce(w, x, ws, y)
         ref = L.lutgemm_gemv(w, x)
         torch.cuda.synchronize()
+        assert_parity(y.float().cpu().numpy(), O.bcq_gemv(d["planes"], d["alpha"], None, gen_x(r, 1, n), n, g),
+                      ("p2p cols", r))
         assert torch.equal(y.view(torch.int16), ref.view(torch.int16))  # one slot: the fp16 of the same fp32 row
     grp.close()
 
@@ -63,6 +70,7 @@ def test_p2p_world1_uniform_offset_formats(mode, compact):
                                torch.from_numpy(u["zero"]).cuda(), q, g, compact=compact)
     grp = L.P2PGroup(0, 1, m, out_bytes=4 * m)
     ws = L.make_workspace(L.lutgemm_workspace_bytes(m, n, 1), "cuda")
+    planes, alpha, z = O.uniform_to_bcq(u["codes"], u["scale"], u["zero"], q)
     for r in range(3):
         x = torch.from_numpy(gen_x(20 + r, 1, n)[0]).cuda()
         y = torch.empty(m, dtype=torch.float16, device="cuda")
@@ -72,6 +80,9 @@ def test_p2p_world1_uniform_offset_formats(mode, compact):
             grp.gemv_allreduce(w, x, ws, y)
         ref = L.lutgemm_gemv(w, x)
         torch.cuda.synchronize()
+        assert_parity(y.float().cpu().numpy(),
+                      O.bcq_gemv(planes, O.store_fp16(alpha), O.store_fp16(z), gen_x(20 + r, 1, n), n, g),
+                      (mode, compact, r))
         assert torch.equal(y.view(torch.int16), ref.view(torch.int16))
     grp.close()
 

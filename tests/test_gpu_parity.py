@@ -7,7 +7,7 @@ import pytest
 import torch
 
 import oracle as O
-from tests._helpers import assert_parity, parity
+from tests._helpers import assert_parity, oracle_rows_parallel, parity, stratified_rows
 from workloads import CONFIGS, gen_bcq, gen_uniform, gen_x
 
 pytestmark = pytest.mark.gpu
@@ -155,7 +155,36 @@ def _sampled_rows(m, seed, k=192):
     return np.array(sorted(r for r in rows if 0 <= r < m))
 
 
-@pytest.mark.parametrize("name", ["fc1", "fc2", "attn"])
+@pytest.mark.parametrize("name", ["fc1", "fc2"])
+def test_full_size_gemv_all_rows(name):
+    """BASELINE config 3 at full size, b = 1, in the launch configuration bench.py times: EVERY
+    output row against the fp64 oracle (row blocks evaluated in parallel worker processes)."""
+    c = CONFIGS[name]
+    d = gen_bcq(c["seed"], c["m"], c["n"], c["q"], c["g"])
+    X = gen_x(c["seed"], 1, c["n"])
+    y = run(pack(d), X)
+    ref = oracle_rows_parallel(d["planes"], d["alpha"], None, X, c["n"], c["g"])
+    p = assert_parity(y, ref, name)
+    print(f"{name} all {c['m']} rows: {p}")
+
+
+@pytest.mark.parametrize("b", [2, 4, 8, 16])
+@pytest.mark.parametrize("name", ["fc1", "fc2"])
+def test_ffn_batched_stratified_rows(name, b):
+    """Config 3 batched at full size: 4 rows from every 256-row block (every reducer range and
+    row block of the batched kernels) against the fp64 oracle, every batch row."""
+    c = CONFIGS[name]
+    d = gen_bcq(c["seed"], c["m"], c["n"], c["q"], c["g"])
+    X = gen_x(c["seed"] + b, b, c["n"])
+    Y = run(pack(d), X)
+    rows = stratified_rows(c["m"], per_block=4, seed=b)
+    ref = oracle_rows_parallel(d["planes"], d["alpha"], None, X, c["n"], c["g"], rows, block=128)
+    for beta in range(b):
+        assert_parity(Y[beta, rows], ref[beta], (name, b, beta))
+    assert_parity(Y[:, rows].ravel(), ref.ravel(), (name, b))
+
+
+@pytest.mark.parametrize("name", ["attn"])
 def test_full_size_gemv_sampled_rows(name):
     """BASELINE full sizes, in the launch configuration bench.py times."""
     c = CONFIGS[name]
@@ -206,8 +235,8 @@ def test_fc1_batched_32_sampled():
     d = gen_bcq(c["seed"], c["m"], c["n"], c["q"], c["g"])
     X = gen_x(c["seed"], 32, c["n"])
     Y = run(pack(d), X)
-    rows = _sampled_rows(c["m"], 7, k=64)
-    ref = O.bcq_gemv_rows(d["planes"], d["alpha"], None, X, c["n"], c["g"], rows)
+    rows = stratified_rows(c["m"], per_block=1, seed=7)
+    ref = oracle_rows_parallel(d["planes"], d["alpha"], None, X, c["n"], c["g"], rows, block=64)
     assert_parity(Y[:, rows], ref, "fc1-b32")
 
 

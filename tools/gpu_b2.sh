@@ -1,5 +1,5 @@
 set -e
-python -c "import __graft_entry__ as g; g.build()"
+python paper_2206_09557_b200/_build.py
 set +e
 timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "batched or random or compact or metamorphic" 2>&1 | tail -4
 for X in 0 1; do

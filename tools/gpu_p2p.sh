@@ -1,7 +1,7 @@
 #!/bin/bash
 # P2P tests (rows all-gather and column all-reduce) on one GPU, plus world-1 timing
 mkdir -p gpurun_out
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/p2p_build.log 2>&1
+python paper_2206_09557_b200/_build.py > gpurun_out/p2p_build.log 2>&1
 timeout 900 python -m pytest tests/test_gpu_p2p.py -q -x > gpurun_out/p2p_tests.log 2>&1
 echo "pytest exit $?" >> gpurun_out/p2p_tests.log
 timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node=2 --master-addr 127.0.0.1 --master-port 29561 \
