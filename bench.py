@@ -249,6 +249,28 @@ def run_reference(args, cfg) -> None:
 # GPU arm
 # ---------------------------------------------------------------------------
 
+def _timed_graph(step, G: int, reps: int, warm: int, stream):
+    """Capture G consecutive steps in one CUDA graph; replay `warm` times untimed, then `reps` times
+    between CUDA events on `stream`.  Returns (total ms, per-replay ms list)."""
+    import torch
+    graph = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream()
+    cap.wait_stream(stream)
+    with torch.cuda.graph(graph, stream=cap):
+        for i in range(G):
+            step(i)
+    for _ in range(max(1, warm)):
+        graph.replay()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+    ev[0].record(stream)
+    for r in range(reps):
+        graph.replay()
+        ev[r + 1].record(stream)
+    torch.cuda.synchronize()
+    return ev[0].elapsed_time(ev[-1]), [ev[r].elapsed_time(ev[r + 1]) for r in range(reps)], graph
+
+
 def run_gpu(args, cfg) -> None:
     import torch
 
@@ -258,142 +280,165 @@ def run_gpu(args, cfg) -> None:
     import paper_2206_09557_b200 as L
     from workloads import gen_bcq, gen_x
 
+    comm = p2p = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
         comm = L.TPComm(rank, world, device=dev)
+    mode = args.tp_mode
     m, n, q, g = cfg["m"], cfg["n"], cfg["q"], cfg["g"]
-    d = gen_bcq(cfg["seed"] + 1000 * rank, m, n, q, g)
-    x_host = gen_x(cfg["seed"], 1, n)
+    if mode == "rows":  # m-split: rank r owns rows [r m/N, (r+1) m/N) and sees the full x
+        if m % (8 * world):
+            raise SystemExit(f"m={m} must split into {world} shards of a multiple of 8 rows")
+        ms, ns = m // world, n
+    else:  # n-split: rank r owns columns [r n/N, (r+1) n/N) (multiple of g) and x's slice
+        if n % (world * g):
+            raise SystemExit(f"n={n} must split into {world} shards of whole groups of {g}")
+        ms, ns = m, n // world
+    d = gen_bcq(cfg["seed"] + 1000 * rank, ms, ns, q, g)  # this rank's shard (seeded per rank)
+    x_full = gen_x(cfg["seed"], 1, n)
+    x_host = x_full if mode == "rows" else x_full[:, rank * ns:(rank + 1) * ns]
     planes = torch.from_numpy(d["planes"].view(np.int32)).to(dev)
     alpha = torch.from_numpy(d["alpha"]).to(dev)
-    B = algorithmic_bytes(m, n, q, g)
+    B = algorithmic_bytes(m, n, q, g)            # the whole layer (all ranks)
+    Bs = algorithmic_bytes(ms, ns, q, g)         # this rank's shard
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-    ncopies = max(2, math.ceil(3 * l2 / B))
-    ws_list = [L.lutgemm_pack_bcq(planes, alpha, None, n, g) for _ in range(ncopies)]
+    ncopies = max(2, math.ceil(3 * l2 / Bs))
+    ws_list = [L.lutgemm_pack_bcq(planes, alpha, None, ns, g) for _ in range(ncopies)]
     del planes, alpha
-    x = torch.from_numpy(x_host[0]).to(dev)
-    y = torch.empty(m * world, dtype=torch.float16, device=dev)
-    wsb = L.lutgemm_workspace_bytes(m, n, 1)
-    ws = L.make_workspace(wsb, dev)
+    x = torch.from_numpy(np.ascontiguousarray(x_host[0])).to(dev)
+    y = torch.empty(m, dtype=torch.float16, device=dev)        # full (replicated) output
+    y_local = torch.empty(ms, dtype=torch.float16, device=dev)
+    ws = L.make_workspace(L.lutgemm_workspace_bytes(ms, ns, 1), dev)
     stream = torch.cuda.current_stream()
+    tp_mode = L.TP_ROWS_ALLGATHER if mode == "rows" else L.TP_COLS_ALLREDUCE
     if world > 1:
-        tws = L.make_workspace(comm.workspace_bytes(L.TP_ROWS_ALLGATHER, m, n, 1), dev)
-        p2p = L.P2PGroup(rank, world, m * world) if args.tp_impl == "p2p" else None
+        tws = L.make_workspace(comm.workspace_bytes(tp_mode, ms, ns, 1), dev)
+        if args.tp_impl == "p2p":
+            p2p = L.P2PGroup(rank, world, rows_out=m if mode == "rows" else 0, cols_m=m if mode == "cols" else 0)
 
     def step(i):
         w = ws_list[i % ncopies]
-        if world > 1 and p2p is not None:  # fused all-gather in the GEMV epilogue (NEXT-1)
-            p2p.gemv_allgather(w, x, ws)
-        elif world > 1:
-            comm.linear(L.TP_ROWS_ALLGATHER, w, x, y, tws)
-        else:
+        if world == 1:
             L.lutgemm_gemv(w, x, y, ws)
+        elif p2p is not None:  # exchange fused into the GEMV epilogue over peer memory (NEXT-1)
+            (p2p.gemv_allgather if mode == "rows" else p2p.gemv_allreduce)(w, x, ws, y)
+        else:  # GEMV + NCCL collective (lutgemm_tp_linear)
+            comm.linear(tp_mode, w, x, y, tws)
+
+    def gemv_only(i):  # the shard's product without the exchange
+        L.lutgemm_gemv(ws_list[i % ncopies], x, y_local, ws)
 
     def barrier():
         if world > 1:
+            comm.wait(stream)  # polls NCCL for asynchronous errors instead of blocking blindly
             torch.distributed.barrier(device_ids=[local])
         torch.cuda.synchronize()
+
+    def max_over_ranks(vals):
+        if world == 1:
+            return vals
+        t = torch.tensor(vals, dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return t.tolist()
 
     for i in range(max(args.warmup, 3)):
         step(i)
     barrier()
-    use_graph = not args.no_graph and world == 1
-    if use_graph:
-        # the timed region replays a CUDA graph of G consecutive GEMVs (rotating
-        # weight copies); PDL edges let each GEMV's weight streaming start under
-        # the previous one's tail, as in a decoder's chain of linears
-        G = max(ncopies, min(args.steps, 50) // ncopies * ncopies)
-        reps = max(1, math.ceil(args.steps / G))
-        steps_timed = reps * G
-        graph = torch.cuda.CUDAGraph()
-        cap = torch.cuda.Stream()
-        cap.wait_stream(stream)
-        n0 = L.lutgemm_launch_count()
-        with torch.cuda.graph(graph, stream=cap):
-            for i in range(G):
-                step(i)
-        launches_per_step = (L.lutgemm_launch_count() - n0) / G
-        for _ in range(max(1, math.ceil(args.warmup / G))):
-            graph.replay()
-        barrier()
-    else:
-        steps_timed = args.steps
-        n0 = L.lutgemm_launch_count()
-        step(0)
-        launches_per_step = L.lutgemm_launch_count() - n0
-    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # the timed region replays a CUDA graph of G consecutive steps (rotating weight copies); PDL
+    # edges let each GEMV's weight streaming start under the previous one's tail, as in a
+    # decoder's chain of linears
+    G = max(ncopies, min(args.steps, 50) // ncopies * ncopies)
+    reps = max(1, math.ceil(args.steps / G))
+    steps_timed = reps * G
+    n0 = L.lutgemm_launch_count()
     sampler = ClockSampler(local)
     barrier()
-    # events between consecutive graph replays (no gap: recorded on the same stream)
-    rep_ev = [torch.cuda.Event(enable_timing=True) for _ in range((reps if use_graph else 0) + 1)]
     with sampler:
-        t_start.record(stream)
-        if use_graph:
-            rep_ev[0].record(stream)
-            for r in range(reps):
-                graph.replay()
-                rep_ev[r + 1].record(stream)
-        else:
-            for i in range(args.steps):
-                step(i)
-        t_end.record(stream)
-        torch.cuda.synchronize()
+        total_ms, per_rep, graph = _timed_graph(step, G, reps, max(1, math.ceil(args.warmup / G)), stream)
+    launches_per_step = (L.lutgemm_launch_count() - n0) / G
+    del graph
     barrier()
-    total_ms = t_start.elapsed_time(t_end)
-    dist = None
-    if use_graph and reps >= 3:
-        per = np.array([rep_ev[r].elapsed_time(rep_ev[r + 1]) for r in range(reps)]) / G * 1e3  # us per GEMV
-        dist = {"p10": round(float(np.percentile(per, 10)), 3), "median": round(float(np.median(per)), 3),
-                "p90": round(float(np.percentile(per, 90)), 3), "replays": int(reps), "gemvs_per_replay": int(G)}
-    # per-launch events on the launching stream (one GEMV = one LUT kernel with the fused reduction)
+    dist_us = None
+    if reps >= 3:
+        per = np.array(per_rep) / G * 1e3
+        dist_us = {"p10": round(float(np.percentile(per, 10)), 3), "median": round(float(np.median(per)), 3),
+                   "p90": round(float(np.percentile(per, 90)), 3), "replays": int(reps), "gemvs_per_replay": int(G)}
+    # the shard GEMV alone in the same graph style (TP: exchange cost = step - GEMV)
+    gemv_ms = None
+    if world > 1:
+        barrier()
+        gemv_ms, _, gg = _timed_graph(gemv_only, G, reps, 1, stream)
+        del gg
+    # isolated launches: events around each eager call (no overlap with a neighbour)
     ne = min(args.steps, 200)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(ne)]
+    barrier()
     for i in range(ne):
         ev[i][0].record(stream)
         step(i)
         ev[i][1].record(stream)
     torch.cuda.synchronize()
-    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
-    if world > 1:
-        t = torch.tensor([total_ms, kern_ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms, kern_ms = float(t[0]), float(t[1])
+    iso_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    total_ms, iso_ms, gemv_ms_v = max_over_ranks([total_ms, iso_ms, gemv_ms if gemv_ms is not None else 0.0])
     ms_per_step = total_ms / steps_timed
-    value = B * world / (ms_per_step * 1e-3) / 1e9
+    value = B / (ms_per_step * 1e-3) / 1e9  # whole-layer bytes over the step time (max over ranks)
 
-    # correctness guard on the timed configuration (sampled rows vs the oracle)
+    # correctness guard on the timed configuration: sampled rows vs the oracle (every rank's shard)
     parity = None
-    if rank == 0 and not args.no_check:
+    if not args.no_check:
         import oracle as O
-        L.lutgemm_gemv(ws_list[0], x, y[:m], ws)
+        step(0)
         torch.cuda.synchronize()
-        rows = np.linspace(0, m - 1, 64).astype(int)
-        ref = O.bcq_gemv_rows(d["planes"], d["alpha"], None, x_host, n, g, rows)[0]
-        got = y[:m].float().cpu().numpy()[rows].astype(np.float64)
-        parity = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+        got_all = y.float().cpu().numpy().astype(np.float64)
+        rows_local = np.linspace(0, ms - 1, 64).astype(int)
+        if mode == "rows":
+            ref = O.bcq_gemv_rows(d["planes"], d["alpha"], None, x_host, ns, g, rows_local)[0]
+            got = got_all[rank * ms + rows_local]
+            err2, ref2 = float(np.sum((got - ref) ** 2)), float(np.sum(ref ** 2))
+        else:  # y = sum over ranks of each shard's partial: sum the fp64 oracle partials across ranks
+            part = O.bcq_gemv_rows(d["planes"], d["alpha"], None, x_host, ns, g, rows_local)[0]
+            if world > 1:
+                t = torch.tensor(part, dtype=torch.float64, device=dev)
+                torch.distributed.all_reduce(t)
+                part = t.cpu().numpy()
+            got = got_all[rows_local]
+            err2, ref2 = float(np.sum((got - part) ** 2)), float(np.sum(part ** 2))
+        if world > 1:
+            t = torch.tensor([err2, ref2], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t)
+            err2, ref2 = float(t[0]), float(t[1])
+        parity = math.sqrt(err2 / ref2)
 
-    # e2e: host (pinned) x -> device -> GEMV -> host y, through the C ABI
+    # e2e through the public API: pinned host x -> device -> product (+ exchange) -> pinned host y
     e2e = None
+    xh = torch.from_numpy(np.ascontiguousarray(x_host)).pin_memory()
+    yh = torch.empty((1, m), dtype=torch.float16).pin_memory()
+    ke = max(10, min(args.steps, 2000))
     if world == 1:
-        hb = L.lutgemm_host_workspace_bytes(m, n, 1)
-        hws = L.make_workspace(hb, dev)
-        xh = torch.from_numpy(x_host).pin_memory()
-        yh = torch.empty((1, m), dtype=torch.float16).pin_memory()
-        for i in range(3):
-            L.lutgemm_gemm_host(ws_list[i % ncopies], xh, yh, hws)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ke = max(10, min(args.steps, 2000))
-        torch.cuda.synchronize()
-        e0.record(stream)
-        for i in range(ke):
-            L.lutgemm_gemm_host(ws_list[i % ncopies], xh, yh, hws)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e_ms = e0.elapsed_time(e1) / ke
-        e2e = {"value": round(B / (e_ms * 1e-3) / 1e9, 2), "unit": UNIT, "h2d_bytes_per_step": 2 * n,
-               "d2h_bytes_per_step": 2 * m, "us_per_step": round(e_ms * 1e3, 3), "steps": ke,
-               "api": "lutgemm_gemm_host (C ABI, pinned host buffers, stream-synchronous)"}
+        hws = L.make_workspace(L.lutgemm_host_workspace_bytes(m, n, 1), dev)
+        e2e_step = lambda i: L.lutgemm_gemm_host(ws_list[i % ncopies], xh, yh, hws)  # noqa: E731
+        api = "lutgemm_gemm_host (C ABI, pinned host buffers, stream-synchronous)"
+    else:
+        def e2e_step(i):
+            x.copy_(xh[0], non_blocking=True)
+            step(i)
+            yh[0].copy_(y, non_blocking=True)
+            stream.synchronize()
+        api = (f"H2D x -> {'P2PGroup' if p2p is not None else 'TPComm.linear'} -> D2H y, pinned buffers, "
+               "stream-synchronous, every rank")
+    for i in range(3):
+        e2e_step(i)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(ke):
+        e2e_step(i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    (e_ms,) = max_over_ranks([e0.elapsed_time(e1) / ke])
+    e2e = {"value": round(B / (e_ms * 1e-3) / 1e9, 2), "unit": UNIT, "h2d_bytes_per_step": 2 * ns,
+           "d2h_bytes_per_step": 2 * m, "us_per_step": round(e_ms * 1e3, 3), "steps": ke, "api": api}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -405,31 +450,35 @@ def run_gpu(args, cfg) -> None:
     box = box_copy_gbs(dev) if rank == 0 else None
     if rank == 0:
         peaks = measured_peaks()
-        achieved = B / (ms_per_step * 1e-3) / 1e9  # per GEMV in the timed (graph) region
-        kname = "lut_gemv_kernel"
+        per_gpu = Bs / (ms_per_step * 1e-3) / 1e9  # this rank's shard bytes over the step time
+        layer = ("fc1 (OPT-175B FFN-1: in 12288 -> out 49152)" if cfg["name"] == "fc1" else
+                 "fc2 (OPT-175B FFN-2: in 49152 -> out 12288)" if cfg["name"] == "fc2" else cfg["name"])
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": steps_timed,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 6), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded uniform random bit-planes, alpha ~ 0.87*2^-i*U(.75,1.25)/sqrt(n), x ~ N(0,1) fp16)",
-            "config": {"workload": cfg["name"] + " (OPT-175B FFN-1: in 12288 -> out 49152)", "m": m, "n": n, "q": q,
-                       "g": g, "b": 1,
-                       "parallelism": (f"tp{world} rows+allgather ({args.tp_impl})" if world > 1 else "single GPU"),
-                       "l2": f"{ncopies} rotating weight copies = {ncopies * B / 1e6:.0f} MB > 3x L2 ({l2 / 1e6:.0f} MB)",
+            "config": {"workload": layer, "m": m, "n": n, "q": q, "g": g, "b": 1,
+                       "parallelism": (f"tp{world} {mode} split + {'all-gather' if mode == 'rows' else 'all-reduce'} "
+                                       f"({args.tp_impl})" if world > 1 else "single GPU"),
+                       "shard": [ms, ns],
+                       "l2": f"{ncopies} rotating weight copies per rank = {ncopies * Bs / 1e6:.0f} MB > 3x L2 "
+                             f"({l2 / 1e6:.0f} MB)",
                        "bytes_alg_per_gemv": B},
             "us_per_gemv": round(ms_per_step * 1e3, 3),
-            "us_per_gemv_dist": dist,
-            "pct_of_peak_hbm": round(100 * value / world / peaks["hbm_gbs"], 2),
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": load_traffic_profile(kname),
+            "us_per_gemv_dist": dist_us,
+            "pct_of_peak_hbm": round(100 * per_gpu / peaks["hbm_gbs"], 2),
+            "roofline": {"bound": "hbm", "achieved": round(per_gpu, 2), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": round(per_gpu / peaks["hbm_gbs"], 4), "traffic": load_traffic_profile("lut_gemv_kernel"),
                          "kernel": "lut_gemv_kernel (cross-slice reduction fused; one launch per GEMV)",
                          "kernel_us": round(ms_per_step * 1e3, 3),
-                         "eager_us_per_gemv": round(kern_ms * 1e3, 3),
-                         "timing": "CUDA graph of consecutive GEMVs, events around the replays" if use_graph
-                         else "eager launches, events around the timed region",
-                         "peak_source": peaks["source"], "frac_of_nominal_8TBs": round(achieved / 8000.0, 4),
+                         "isolated_us_per_gemv": round(iso_ms * 1e3, 3),
+                         "frac_isolated": round(Bs / (iso_ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
+                         "timing": "CUDA graph of consecutive steps, events around the replays (chain); "
+                                   "isolated = events around each eager launch",
+                         "peak_source": peaks["source"], "frac_of_nominal_8TBs": round(per_gpu / 8000.0, 4),
                          "box_copy_gbs": None if box is None else round(box, 1),
-                         "frac_of_box_copy": None if box is None else round(achieved / box, 4)},
+                         "frac_of_box_copy": None if box is None else round(per_gpu / box, 4)},
             "clocks": sampler.summary(),
             "e2e": e2e,
             "gpu_launches": int(round(launches_per_step * steps_timed)),
@@ -437,6 +486,10 @@ def run_gpu(args, cfg) -> None:
             "cpu_baseline": cpu,
             "parity_rel_l2_sampled": parity,
         }
+        if world > 1:
+            line["tp"] = {"per_gpu_gbs": round(per_gpu, 2), "shard_gemv_us": round(gemv_ms_v / steps_timed * 1e3, 3),
+                          "exchange_us": round((total_ms - gemv_ms_v) / steps_timed * 1e3, 3),
+                          "impl": args.tp_impl}
         print(json.dumps(line), flush=True)
     if world > 1:
         if p2p is not None:
@@ -451,16 +504,20 @@ def main():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="lutgemm", choices=["lutgemm", "reference"])
-    ap.add_argument("--config", default="fc1")
+    ap.add_argument("--config", default=None, help="workload (default fc1; fc2 for --tp-mode cols)")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-budget", type=float, default=120.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-check", action="store_true")
-    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
+    ap.add_argument("--tp-mode", default="rows", choices=["rows", "cols"],
+                    help="N > 1: rows = m-split + all-gather (fc1); cols = n-split + all-reduce (default config fc2)")
     ap.add_argument("--tp-impl", default="nccl", choices=["nccl", "p2p"],
-                    help="N > 1: GEMV + ncclAllGather, or the all-gather fused into the GEMV epilogue over peer memory")
+                    help="N > 1: GEMV + NCCL collective, or the exchange fused into the GEMV epilogue over peer "
+                         "memory (NEXT-1; validated with processes sharing one GPU, not yet on NVLink)")
     args = ap.parse_args()
     from workloads import CONFIGS
+    if args.config is None:
+        args.config = "fc2" if args.tp_mode == "cols" else "fc1"
     cfg = dict(CONFIGS[args.config], name=args.config)
     if args.impl == "reference":
         run_reference(args, cfg)

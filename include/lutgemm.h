@@ -252,51 +252,59 @@ lutgemm_status lutgemm_tp_linear(lutgemm_tp* tp, int mode, const lutgemm_weight*
                                  const uint16_t* x, int b, uint16_t* y, void* ws, size_t ws_bytes,
                                  void* stream);
 lutgemm_status lutgemm_tp_destroy(lutgemm_tp* tp);
+/* Failure detection (host polling): LUTGEMM_ERR_NCCL with the text of the error if the
+ * communicator hit an asynchronous error (e.g. a peer died), else LUTGEMM_OK.  Poll it while
+ * waiting for a stream that runs collectives, so a broken collective does not hang silently. */
+lutgemm_status lutgemm_tp_async_error(lutgemm_tp* tp);
+/* Abort the communicator (unblocks kernels stuck in its collectives) and free the handle. */
+lutgemm_status lutgemm_tp_abort(lutgemm_tp* tp);
 int lutgemm_tp_rank(const lutgemm_tp* tp);
 int lutgemm_tp_nranks(const lutgemm_tp* tp);
 
-/* ---------------- Fused rows all-gather over peer memory ----------------
- * The tensor-parallel GEMV of ROWS_ALLGATHER with the collective fused into the
- * GEMV's epilogue: the reducer CTAs of rank r store each finished row of its
- * shard straight into every rank's output buffer over NVLink / NVSwitch (CUDA
- * IPC mappings), the grid's last reducer signals every rank at system scope
- * and keeps the grid open until the rank holds all P signals of the round, so
- * the kernel's completion means "gathered output ready".  No NCCL call; one
- * process per GPU.
- *
- * Each rank owns two output buffers (double buffer) and a signal counter.  The
- * output of a call stays valid until the call after next (flow control: a rank
- * overwrites a buffer only after every peer has signalled the round in between,
- * which that peer does after its stream ran everything queued before it).
- * Every rank must make the same sequence of calls.  Not CUDA-graph capturable
- * (the buffer parity and the wait target are host-side round counts). */
+/* ---------------- Tensor-parallel exchange fused into the GEMV ----------------
+ * The collectives of lutgemm_tp_linear's ROWS_ALLGATHER and COLS_ALLREDUCE modes fused into
+ * the GEMV's epilogue over peer memory (CUDA IPC mappings over NVLink / NVSwitch), no NCCL call;
+ * one process per GPU (communication limits tensor parallelism once the matmul is
+ * fast).  A call is ONE kernel on `stream`: the exchange runs in the fused GEMV's epilogue, in
+ * the reducer CTAs (16-byte stores, system-scope release/acquire signals):
+ *  - ROWS (m-split): each finished fp16 row of this rank's shard goes to y and into every
+ *    peer's exchange window; the CTAs signal every rank, wait for all P signals and copy the
+ *    peers' rows from the local window into y.
+ *  - COLS (n-split): reduce-scatter + all-gather.  Rank o owns rows [o mb, (o+1) mb),
+ *    mb = 8 ceil(ceil(m/P)/8); the reducers store this rank's fp32 partial rows into the
+ *    owner's window only, signal, wait; each rank sums its owned block over the P slots in rank
+ *    order (deterministic, bitwise identical on every rank, within tolerance of the 1-GPU
+ *    result), rounds to fp16 and stores the block into y and every peer's window, signals,
+ *    waits and copies the peers' blocks into y.
+ * The round number lives on the device, so calls are CUDA-graph capturable; each rank owns two
+ * windows (double buffer) and 64-bit signal counters.  Every rank must make the same sequence of
+ * calls on a group.  y is complete when the call's kernel completes on the stream. */
 typedef struct lutgemm_p2p lutgemm_p2p;
 
-/* Allocate this rank's buffers (two of out_bytes, device) and signal counter
- * and write a 256-byte exchange record (CUDA IPC handles, rank, sizes) that the
- * caller gathers from all ranks, in rank order, by any transport. 1 <= nranks <= 8. */
-lutgemm_status lutgemm_p2p_create(int rank, int nranks, size_t out_bytes, lutgemm_p2p** out, uint8_t record[256]);
-/* Open the peers' buffers from the gathered records [nranks][256]. */
+/* Bytes of one exchange window for `mode` (LUTGEMM_TP_ROWS_ALLGATHER: m = rows of the gathered
+ * output, P * m_shard; LUTGEMM_TP_COLS_ALLREDUCE: m = rows of the layer); 0 on bad arguments.
+ * A group serves every call whose need is <= its window size. */
+size_t lutgemm_p2p_window_bytes(int nranks, int mode, int m);
+/* Allocate this rank's two windows (win_bytes each, device) and signal block and write a 256-byte
+ * exchange record (CUDA IPC handles, rank, sizes) that the caller gathers from all ranks, in rank
+ * order, by any transport.  1 <= nranks <= 8.  Collective in the sense that every rank creates
+ * one group with the same win_bytes. */
+lutgemm_status lutgemm_p2p_create(int rank, int nranks, size_t win_bytes, lutgemm_p2p** out, uint8_t record[256]);
+/* Open the peers' windows from the gathered records [nranks][256]; once per group (a second call
+ * is rejected; on failure every mapping it opened is closed). */
 lutgemm_status lutgemm_p2p_connect(lutgemm_p2p* g, const uint8_t* records);
-/* y_full [P * m_shard] (fp16) = the rows of every rank's shard times x, gathered
- * into this rank's current output buffer, returned in *y_full (may be NULL);
- * if y_copy (device) is not NULL the result is also copied there on `stream`.
- * shard: this rank's rows [r m_shard, (r+1) m_shard) of W, packed; x [n] fp16
- * (16-byte aligned); ws >= lutgemm_workspace_bytes(m_shard, n, 1).  The shard
- * must run the fused GEMV mode (LUTGEMM_ERR_UNSUPPORTED otherwise: too few row
- * quads for the J CTAs per slice, or more slices than SMs). */
+/* ROWS: y [P * m_shard] (fp16, device, caller-owned, 2-byte aligned) = every rank's shard rows
+ * times x.  shard: this rank's rows [r m_shard, (r+1) m_shard) of W, packed, m_shard % 8 == 0;
+ * x [n] fp16 (16-byte aligned); ws >= lutgemm_workspace_bytes(m_shard, n, 1).  The shard must run
+ * the fused GEMV mode (LUTGEMM_ERR_UNSUPPORTED otherwise: too few row quads for the J CTAs per
+ * slice, or more slices than SMs).  Validated like lutgemm_gemv. */
 lutgemm_status lutgemm_p2p_gemv_allgather(lutgemm_p2p* g, const lutgemm_weight* shard, const uint16_t* x, void* ws,
-                                          size_t ws_bytes, void* stream, uint16_t** y_full, uint16_t* y_copy);
-/* Column split (Megatron's second linear): y [m] (fp16, device, caller-owned)
- * = sum over ranks of (shard_r [m][n/P]) x_r, x_r = this rank's slice of x.
- * The fused GEMV's reducers store this rank's fp32 partial rows into slot
- * `rank` of every rank's current buffer (P2P), signal as above, and a small
- * kernel then sums the P slots of this rank in rank order (deterministic,
- * within tolerance of the 1-GPU result) and rounds to fp16.  Buffers must hold
- * P * m fp32 (out_bytes >= 4 P m). */
+                                          size_t ws_bytes, void* stream, uint16_t* y);
+/* COLS: y [m] (fp16, device) = sum over ranks of (shard_r [m][n/P]) x_r, x_r = this rank's slice of
+ * x [n/P] (columns aligned to g).  Same requirements as above. */
 lutgemm_status lutgemm_p2p_gemv_allreduce(lutgemm_p2p* g, const lutgemm_weight* shard, const uint16_t* x, void* ws,
                                           size_t ws_bytes, void* stream, uint16_t* y);
-/* Synchronises the device, closes the peer mappings and frees the buffers. */
+/* Synchronises the group's device, closes the peer mappings and frees the windows. */
 lutgemm_status lutgemm_p2p_destroy(lutgemm_p2p* g);
 
 #ifdef __cplusplus

@@ -19,7 +19,7 @@ namespace lg {
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMiscBytes = 8192;       // x double buffer (2 x 2 KB) + mbarriers + flags
-constexpr int kSmemBytes = 3 * 65536;  // LUT (128 KB) on a 64 KB boundary + misc, for any base
+constexpr int kSmemBytes = 227 * 1024;  // LUT (128 KB) on a 64 KB boundary + misc + weight prefetch area
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kFusedMaxJ = 256;        // max CTAs per slice in the fused-reduction mode
 
@@ -27,13 +27,26 @@ struct SmemMap {
   uint32_t lut;     // shared-window address of the LUT (multiple of 64 KB)
   uint32_t misc;    // shared-window address of the misc block
   uint8_t* misc_p;  // generic pointer to the misc block
+  uint32_t fa, fa_bytes, fb, fb_bytes;  // the two free areas (weight prefetch), 16-byte aligned
 };
 
 __device__ __forceinline__ SmemMap map_smem(uint8_t* smem) {
   SmemMap m;
-  const uint32_t base = smem_u32(smem);
+  const uint32_t base = smem_u32(smem), end = base + (uint32_t)kSmemBytes;
   m.lut = (base + 0xFFFFu) & ~0xFFFFu;
-  m.misc = (m.lut - base >= (uint32_t)kMiscBytes) ? base : m.lut + kLutBytes;
+  if (m.lut - base >= (uint32_t)kMiscBytes) {  // [base, misc) [.. free A ..) [LUT) [.. free B ..)
+    m.misc = base;
+    m.fa = base + kMiscBytes;
+    m.fb = m.lut + kLutBytes;
+  } else {                                      // [small gap) [LUT) [misc) [.. free B ..)
+    m.misc = m.lut + kLutBytes;
+    m.fa = base;
+    m.fb = m.misc + kMiscBytes;
+  }
+  m.fa = (m.fa + 15u) & ~15u;
+  m.fb = (m.fb + 15u) & ~15u;
+  m.fa_bytes = m.lut > m.fa ? m.lut - m.fa : 0u;
+  m.fb_bytes = end > m.fb ? end - m.fb : 0u;
   m.misc_p = smem + (m.misc - base);
   return m;
 }

@@ -291,5 +291,7 @@ size_t lutgemm_trace_read(uint64_t* host, size_t n) {
 
 }  // extern "C"
 
-// exported for the TP translation unit
+// exported for the TP / P2P translation units
 lutgemm_status lutgemm_internal_fail(lutgemm_status st, const char* msg) { return fail(st, "%s", msg); }
+lutgemm_status lutgemm_internal_check_weight(const lutgemm_weight* w) { return check_weight(w); }
+lutgemm_status lutgemm_internal_check_device() { return check_device(); }

@@ -94,33 +94,35 @@ static bool fusable(int S, int units, int sms) {
 }
 
 static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint16_t* x, int b, uint16_t* y, float* yf,
-                                  void* ws, cudaStream_t st, __half* const* peer_y, unsigned* const* peer_sig,
-                                  int npeers, int yoff, int self = 0, unsigned target = 0, int f32 = 0);
+                                  void* ws, cudaStream_t st, const P2PArgs* pa);
 
 cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, int b, uint16_t* y, float* yf,
                         void* ws, cudaStream_t st) {
-  return run_product_ex(sh, data, x, b, y, yf, ws, st, nullptr, nullptr, 0, 0);
+  return run_product_ex(sh, data, x, b, y, yf, ws, st, nullptr);
 }
 
-cudaError_t run_gemv_p2p(const Shape& sh, const void* data, const uint16_t* x, void* ws, __half* const* peer_y,
-                         unsigned* const* peer_sig, int npeers, int yoff, int self, unsigned target, int f32,
-                         cudaStream_t st) {
-  if (npeers < 1 || npeers > 8 || self < 0 || self >= npeers) return cudaErrorInvalidValue;
-  return run_product_ex(sh, data, x, 1, nullptr, nullptr, ws, st, peer_y, peer_sig, npeers, yoff, self, target, f32);
+cudaError_t run_gemv_p2p(const Shape& sh, const void* data, const uint16_t* x, void* ws, const P2PArgs& a,
+                         uint16_t* y, cudaStream_t st) {
+  if (a.npeers < 1 || a.npeers > 8 || a.self < 0 || a.self >= a.npeers || (a.mode != 1 && a.mode != 2))
+    return cudaErrorInvalidValue;
+  return run_product_ex(sh, data, x, 1, y, nullptr, ws, st, &a);
 }
 
 static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint16_t* x, int b, uint16_t* y, float* yf,
-                                  void* ws, cudaStream_t st, __half* const* peer_y, unsigned* const* peer_sig,
-                                  int npeers, int yoff, int self, unsigned target, int f32) {
+                                  void* ws, cudaStream_t st, const P2PArgs* pa) {
   KParams p;
-  p.p2p_f32 = f32;
-  p.npeers = npeers;
-  p.yoff = yoff;
-  p.p2p_self = self;
-  p.p2p_target = target;
+  p.p2p_mode = pa ? pa->mode : 0;
+  p.npeers = pa ? pa->npeers : 0;
+  p.yoff = pa ? pa->yoff : 0;
+  p.p2p_self = pa ? pa->self : 0;
+  p.p2p_mb = pa ? pa->mb : 0;
+  p.p2p_yarea = pa ? pa->yarea : 0;
+  p.p2p_round = pa ? pa->round : nullptr;
   for (int i = 0; i < 8; ++i) {
-    p.peer_y[i] = i < npeers ? peer_y[i] : nullptr;
-    p.peer_sig[i] = i < npeers ? peer_sig[i] : nullptr;
+    const bool on = pa && i < pa->npeers;
+    p.p2p_win[0][i] = on ? pa->win[0][i] : nullptr;
+    p.p2p_win[1][i] = on ? pa->win[1][i] : nullptr;
+    p.p2p_sig[i] = on ? pa->sig[i] : nullptr;
   }
   p.data = static_cast<const uint8_t*>(data);
   p.x = reinterpret_cast<const __half*>(x);
@@ -178,10 +180,17 @@ static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint1
       p.reducers = (int)std::min<long long>(p.s2, (red_bytes + 16383) / 16384);
     }
   }
+  p.fused_pair = pa ? 1 : 0;  // P2P epilogue: 8-row units, so row-quad groups start at even quads
+  {
+    static const int pf = getenv("LUTGEMM_SMEM_PF") ? atoi(getenv("LUTGEMM_SMEM_PF")) : 1 << 20;
+    static const unsigned l2 = getenv("LUTGEMM_L2_PF") ? (unsigned)atoi(getenv("LUTGEMM_L2_PF")) : 0u;
+    p.smem_pf = pf;
+    p.l2_pf = l2;
+  }
   if (!batched) {
     const int sms = num_sms();
     const int J = sh.S <= sms ? sms / sh.S : 0;
-    if (fusable(sh.S, sh.RQ, sms)) {
+    if (fusable(sh.S, pa ? (sh.RQ + 1) / 2 : sh.RQ, sms)) {
       p.fused_J = J;
       grid = sh.S * J;
       const long long red_bytes = (long long)sh.S * 16 * ((sh.RQ + J - 1) / J);
@@ -190,7 +199,7 @@ static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint1
       if (env && atoi(env) > 0) p.reducers = std::min(atoi(env), sh.S);
     }
   }
-  if (npeers > 0 && (batched || p.fused_J <= 0)) return cudaErrorNotSupported;  // the fused epilogue only
+  if (pa && (batched || p.fused_J <= 0)) return cudaErrorNotSupported;  // the fused epilogue only
   cudaError_t e = !batched ? launch_gemv(p, grid, st) : (p.s2 > 0 ? launch_smallb(p, grid, st) : launch_batched(p, grid, st));
   if (e != cudaSuccess) return e;
   if (p.fused_J > 0) return cudaSuccess;  // reduced in-kernel

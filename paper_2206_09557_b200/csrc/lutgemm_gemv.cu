@@ -44,6 +44,194 @@ namespace lg {
 // most a few slices), and lut_reduce_kernel follows.  Inside a segment the 16
 // warps take row quads rq_a + warp + 16 t round-robin.
 // ---------------------------------------------------------------------------
+// first row quad of row-quad group fj of J (fused mode); with `pair` (P2P epilogue) groups start
+// on even quads, so the epilogue's 8-row units never straddle two groups
+__device__ __forceinline__ int group_quad(int RQ, int J, int fj, int pair) {
+  if (!pair) return (int)((long long)RQ * fj / J);
+  return min(RQ, 2 * (int)((long long)((RQ + 1) / 2) * fj / J));
+}
+
+// 8 consecutive fp32 rows [r, r + 8) of the slice partials summed over the S slices in slice
+// order (R11); rows >= m4 read as 0
+__device__ __forceinline__ void sum8_rows(const float* partial, int S, int m4, int r, float (&v)[8]) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v[k] = 0.f;
+  if (r + 8 <= m4) {
+    for (int s = 0; s < S; ++s) {
+      const float4 a = __ldcg(reinterpret_cast<const float4*>(partial + (size_t)s * m4 + r));
+      const float4 b = __ldcg(reinterpret_cast<const float4*>(partial + (size_t)s * m4 + r + 4));
+      v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w;
+      v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
+    }
+  } else {
+    for (int s = 0; s < S; ++s)
+      for (int k = 0; k < 8 && r + k < m4; ++k) v[k] += __ldcg(partial + (size_t)s * m4 + r + k);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Tensor-parallel exchange fused into the GEMV epilogue (NEXT-1, lutgemm_p2p.cu).
+// Runs in the R reducer CTAs of every row-quad group (NRED = J R CTAs, all resident), after the
+// group's slice partials are complete.  Rows of 8-row units [8u, 8u + 8), 16-byte stores.
+//   rows (p2p_mode 1, m-split):  fp16 rows of this rank's shard -> this rank's y (local) and every
+//     peer's window[par] at row yoff + r; signal A; wait for the P signals A; copy the peers' rows
+//     out of the local window into y.
+//   cols (p2p_mode 2, n-split):  fp32 partial rows -> the owner's window[par] slot [self]
+//     (reduce-scatter); signal A; wait; sum the owned block over the P slots in rank order
+//     (deterministic), fp16 -> y (local) and every peer's window y-area; signal B; wait; copy the
+//     peers' blocks out of the local window into y.
+// Signals: the grid's last CTA through a phase (acq_rel counter, gpu scope) issues
+// fence.acq_rel.sys and red.release.sys.u64 on every rank's counter; waits are ld.acquire.sys by
+// thread 0 followed by a CTA barrier (the chain: stores -> bar.sync -> acq_rel RMW -> last CTA's
+// acquire -> fence.sys -> release to the peer -> the peer's acquire -> its bar.sync -> its loads).
+// The last CTA of the final phase advances the device-side round (parity of the double buffer).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 pack_half8(const float (&v)[8]) {
+  uint4 h;
+  h.x = pack_half2(v[0], v[1]);
+  h.y = pack_half2(v[2], v[3]);
+  h.z = pack_half2(v[4], v[5]);
+  h.w = pack_half2(v[6], v[7]);
+  return h;
+}
+
+// store `cnt` (<= 8) fp16 values of h at dst (16-byte store when whole)
+__device__ __forceinline__ void store_half8(uint8_t* dst, const uint4& h, int cnt) {
+  if (cnt >= 8) {
+    *reinterpret_cast<uint4*>(dst) = h;
+  } else {
+    const uint16_t* hs = reinterpret_cast<const uint16_t*>(&h);
+    for (int k = 0; k < cnt; ++k) reinterpret_cast<uint16_t*>(dst)[k] = hs[k];
+  }
+}
+
+// grid-wide phase barrier of the NRED reducer CTAs: the last to arrive (resetting the counter)
+// runs `last` in thread 0; then every CTA waits until its own signal counter reaches `target`
+template <typename F>
+__device__ __forceinline__ void p2p_phase(unsigned* cnt, unsigned nred, const unsigned long long* my_sig,
+                                          unsigned long long target, F last) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (atom_add_acq_rel_u32(cnt, 1u) == nred - 1) {
+      *cnt = 0u;
+      last();
+    }
+    while (ld_acquire_sys_u64(my_sig) < target) __nanosleep(32);
+  }
+  __syncthreads();
+}
+
+// copy units [u0, u1) of 8 fp16 rows from src to dst (both indexed from row 0), rows < rows_end
+__device__ __forceinline__ void copy_rows(__half* dst, const uint8_t* src, int u0, int u1, int rows_end) {
+  for (int u = u0 + (int)threadIdx.x; u < u1; u += kThreads) {
+    const int r = 8 * u;
+    const uint4 v = __ldcg(reinterpret_cast<const uint4*>(src) + u);
+    store_half8(reinterpret_cast<uint8_t*>(dst + r), v, rows_end - r);
+  }
+}
+
+__device__ __forceinline__ void p2p_epilogue(const KParams& p, int J, int R, int fj, int ri, int g0, int g1) {
+  const Shape& sh = p.sh;
+  const int P = p.npeers, self = p.p2p_self;
+  const unsigned nred = (unsigned)(J * R);
+  const int red = fj * R + ri;  // this CTA's index among the reducers
+  unsigned* cnt = p.counters + 2 * kFusedMaxJ;  // 3 phase counters
+  const unsigned long long round = ld_acquire_u64(p.p2p_round);  // previous round complete (PDL wait)
+  const int par = (int)(round & 1ull);
+  const unsigned long long target = (round + 1ull) * (unsigned long long)P;
+  unsigned long long* const* sig = p.p2p_sig;  // sig[pr][0] = A, [1] = B, [2] = round (self only)
+  auto signal_all = [&](int which) {
+    fence_acq_rel_sys();
+    for (int pr = 0; pr < P; ++pr) red_release_sys_add_u64(sig[pr] + which, 1ull);
+  };
+  const int u0g = g0 / 2, u1g = (g1 + 1) / 2;  // the group's 8-row units (groups start on even quads)
+  const int u0 = u0g + (int)((long long)(u1g - u0g) * ri / R), u1 = u0g + (int)((long long)(u1g - u0g) * (ri + 1) / R);
+  auto share = [&](int units, int& a, int& b) {  // this reducer's share of `units` work units
+    a = (int)((long long)units * red / nred);
+    b = (int)((long long)units * (red + 1) / nred);
+  };
+  if (p.p2p_mode == 1) {
+    const int ms = sh.m;
+    for (int u = u0 + (int)threadIdx.x; u < u1; u += kThreads) {
+      const int r = 8 * u;
+      float v[8];
+      sum8_rows(p.partial, sh.S, sh.m4, r, v);
+      const uint4 h = pack_half8(v);
+      store_half8(reinterpret_cast<uint8_t*>(p.y + p.yoff + r), h, ms - r);
+      const size_t off = 2 * (size_t)(p.yoff + r);
+      for (int pr = 0; pr < P; ++pr)
+        if (pr != self) store_half8(p.p2p_win[par][pr] + off, h, ms - r);
+    }
+    p2p_phase(cnt, nred, sig[self], target, [&] { signal_all(0); });
+    // the peers' rows: (P - 1) ms rows out of the local window
+    const int upr = ms / 8;  // ms % 8 == 0 (checked on the host)
+    int a, b;
+    share((P - 1) * upr, a, b);
+    for (int w = a + (int)threadIdx.x; w < b; w += kThreads) {
+      const int k = w / upr, pr = k + (k >= self ? 1 : 0), u = pr * upr + w % upr;
+      const uint4 v = __ldcg(reinterpret_cast<const uint4*>(p.p2p_win[par][self]) + u);
+      *reinterpret_cast<uint4*>(p.y + 8 * u) = v;
+    }
+  } else {
+    const int m = sh.m, mb = p.p2p_mb;
+    for (int u = u0 + (int)threadIdx.x; u < u1; u += kThreads) {
+      const int r = 8 * u;
+      float v[8];
+      sum8_rows(p.partial, sh.S, sh.m4, r, v);
+      const int o = r / mb;
+      float* dst = reinterpret_cast<float*>(p.p2p_win[par][o]) + (size_t)self * mb + (r - o * mb);
+      if (r + 8 <= m) {
+        reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
+        reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
+      } else {
+        for (int k = 0; k < m - r; ++k) dst[k] = v[k];
+      }
+    }
+    p2p_phase(cnt, nred, sig[self], target, [&] { signal_all(0); });
+    // owned block [self mb, self mb + mb): sum the P slots in rank order, fp16 -> y and every peer
+    const float* slots = reinterpret_cast<const float*>(p.p2p_win[par][self]);
+    const int b0 = self * mb, rows = max(0, min(mb, m - b0));
+    int a, b;
+    share((rows + 7) / 8, a, b);
+    for (int w = a + (int)threadIdx.x; w < b; w += kThreads) {
+      const int lr = 8 * w;
+      float v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = 0.f;
+      for (int pr = 0; pr < P; ++pr) {
+        const float4 x0 = __ldcg(reinterpret_cast<const float4*>(slots + (size_t)pr * mb + lr));
+        const float4 x1 = __ldcg(reinterpret_cast<const float4*>(slots + (size_t)pr * mb + lr + 4));
+        v[0] += x0.x; v[1] += x0.y; v[2] += x0.z; v[3] += x0.w;
+        v[4] += x1.x; v[5] += x1.y; v[6] += x1.z; v[7] += x1.w;
+      }
+      const uint4 h = pack_half8(v);
+      store_half8(reinterpret_cast<uint8_t*>(p.y + b0 + lr), h, rows - lr);
+      const size_t off = p.p2p_yarea + 2 * (size_t)(b0 + lr);
+      for (int pr = 0; pr < P; ++pr)
+        if (pr != self) store_half8(p.p2p_win[par][pr] + off, h, rows - lr);
+    }
+    if (P > 1) {
+      p2p_phase(cnt + 1, nred, sig[self] + 1, target, [&] { signal_all(1); });
+      // the peers' blocks out of the local window
+      const int ub = mb / 8;
+      share((P - 1) * ub, a, b);
+      for (int w = a + (int)threadIdx.x; w < b; w += kThreads) {
+        const int k = w / ub, pr = k + (k >= self ? 1 : 0), lu = w % ub;
+        const int r = pr * mb + 8 * lu;
+        if (r >= m) continue;
+        const uint4 v = __ldcg(reinterpret_cast<const uint4*>(p.p2p_win[par][self] + p.p2p_yarea) + r / 8);
+        store_half8(reinterpret_cast<uint8_t*>(p.y + r), v, m - r);
+      }
+    }
+  }
+  // the last reducer to finish advances the round: every reducer has read it by now
+  __syncthreads();
+  if (threadIdx.x == 0 && atom_add_acq_rel_u32(cnt + 2, 1u) == nred - 1) {
+    cnt[2] = 0u;
+    *reinterpret_cast<volatile unsigned long long*>(p.p2p_sig[self] + 2) = round + 1ull;
+  }
+}
+
 template <int QT, int ZM, int PD>
 __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) {
   constexpr bool HAS_Z = ZM != 0, CMP = ZM == 2;
@@ -56,8 +244,8 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
   long long it0, it1;
   if (J > 0) {
     const int fs = blockIdx.x / J, fj = blockIdx.x % J;
-    it0 = (long long)fs * sh.RQ + (long long)sh.RQ * fj / J;
-    it1 = (long long)fs * sh.RQ + (long long)sh.RQ * (fj + 1) / J;
+    it0 = (long long)fs * sh.RQ + group_quad(sh.RQ, J, fj, p.fused_pair);
+    it1 = (long long)fs * sh.RQ + group_quad(sh.RQ, J, fj + 1, p.fused_pair);
   } else {
     it0 = p.items * blockIdx.x / gridDim.x;
     it1 = p.items * (blockIdx.x + 1) / gridDim.x;
@@ -75,11 +263,12 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
   const SmemMap sm = map_smem(smem);
   __half* xbuf0 = reinterpret_cast<__half*>(sm.misc_p);
   __half* xbuf1 = reinterpret_cast<__half*>(sm.misc_p + 2048);
-  const uint32_t bar0 = sm.misc + 4096, bar1 = sm.misc + 4104;
+  const uint32_t bar0 = sm.misc + 4096, bar1 = sm.misc + 4104, bar_pf = sm.misc + 4112;
   const uint32_t lc = (sm.lut & 0xFFFF0000u) | ((uint32_t)(4 * lane + 128) << 8) | (uint32_t)(4 * lane);
   if (tid == 0) {
     mbar_init(bar0, 1);
     mbar_init(bar1, 1);
+    mbar_init(bar_pf, 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -107,16 +296,58 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     const uint8_t* lal = la.ap + (size_t)(rq_a + warp) * la.AB;
     const uint8_t* lz = la.zp + (size_t)(rq_a + warp) * la.ZB;
     int tl = 0;
-    Ring<QT> buf[NB];
-    auto load_quad = [&](Ring<QT>& b) {
-      if (nt == 0) return;  // a warp without quads in the segment loads nothing
-#pragma unroll
-      for (int i = 0; i < QT; ++i) {
-        if (QT <= 4 || i < q) {
-          b.k[i] = ldg_stream_u4(lk + i * la.kstride);
-          if (!CMP || i == 0) b.a[i] = ldg_nc_u2(lal + 8 * i);
+    // Fused mode, first segment: besides the PD register-ring quads, the KEYS (89 % of the bytes at
+    // q = 3, g = 128) of the next NB quads of every warp (quads rq_a + 16 PD .. + 16 (PD + NB)) are
+    // copied into shared memory by the bulk-copy engine at CTA start, before the PDL wait (weights
+    // only), so more of the weight stream is in flight while this CTA waits for the previous
+    // kernel and builds its LUT.  They feed one peeled ring iteration (their scales still come
+    // through the register ring); the quads go to the two free shared-memory areas, TA "rows" of
+    // 16 quads in the first.
+    bool pf = false;
+    uint32_t pfa = 0, pfb = 0;  // lane's key word of the first prefetched quad in area A / area B
+    int TA = 0;
+    if (QT <= 4 && e == 0 && J > 0 && p.smem_pf > 0 && (rq_b - rq_a) >= kWarps * (PD + NB)) {
+      const uint32_t rowb = (uint32_t)kWarps * la.KB;  // bytes of 16 quads' keys
+      TA = min((int)(sm.fa_bytes / rowb), NB);
+      pf = TA + (int)(sm.fb_bytes / rowb) >= NB;
+      if (pf) {
+        const uint32_t lo = (uint32_t)(lane_ok ? lane : 0) * 16u;
+        pfa = sm.fa + lo;
+        pfb = sm.fb + lo;
+        if (tid == 0) {
+          const uint8_t* src = p.data + keys_base(sh, s, Ls) + (size_t)(rq_a + kWarps * PD) * la.KB;
+          mbar_arrive_expect_tx(bar_pf, (uint32_t)NB * rowb);
+          if (TA > 0) bulk_g2s(sm.fa, src, (uint32_t)TA * rowb, bar_pf);
+          if (TA < NB) bulk_g2s(sm.fb, src + (size_t)TA * rowb, (uint32_t)(NB - TA) * rowb, bar_pf);
         }
       }
+      // optional L2 prefetch of the CTA's following key bytes (tuning knob)
+      if (p.l2_pf > 0 && tid == 0) {
+        const size_t kend = keys_base(sh, s, Ls) + (size_t)rq_b * la.KB;
+        const size_t k1 = keys_base(sh, s, Ls) + (size_t)(rq_a + kWarps * (PD + (pf ? NB : 0))) * la.KB;
+        const uint32_t nb = (uint32_t)min((size_t)p.l2_pf, kend > k1 ? kend - k1 : 0) & ~15u;
+        if (nb) bulk_prefetch_l2(p.data + k1, nb);
+      }
+    }
+    Ring<QT> buf[NB];
+    // load quad tl of the warp into b: keys from global memory, or (smem >= 0) from prefetched
+    // row `smem` of the shared-memory area; scales always from global memory
+    auto load_quad = [&](Ring<QT>& b, int smem = -1) {
+      if (nt == 0) return;  // a warp without quads in the segment loads nothing
+      if (smem >= 0) {
+        const uint32_t ka = (smem < TA ? pfa + (uint32_t)smem * kWarps * la.KB
+                                       : pfb + (uint32_t)(smem - TA) * kWarps * la.KB) + (uint32_t)warp * la.KB;
+#pragma unroll
+        for (int i = 0; i < QT; ++i)
+          if (QT <= 4 || i < q) b.k[i] = lds_u4(ka + (uint32_t)i * la.kstride);
+      } else {
+#pragma unroll
+        for (int i = 0; i < QT; ++i)
+          if (QT <= 4 || i < q) b.k[i] = ldg_stream_u4(lk + i * la.kstride);
+      }
+#pragma unroll
+      for (int i = 0; i < QT; ++i)
+        if ((QT <= 4 || i < q) && (!CMP || i == 0)) b.a[i] = ldg_nc_u2(lal + 8 * i);
       if (HAS_Z) b.z = ldg_nc_u2(lz);
       if (++tl < nt) {
         lk += (size_t)kWarps * la.KB;
@@ -171,6 +402,15 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
       pw += 4 * kWarps;
     };
     int t0 = 0;
+    if (pf) {  // peeled first iteration: quads PD .. PD + NB - 1 come from the shared-memory prefetch
+      mbar_wait(bar_pf, 0u);
+#pragma unroll
+      for (int d = 0; d < NB; ++d) {
+        load_quad(buf[(d + PD) % NB], d);
+        quad(buf[d]);
+      }
+      t0 = NB;
+    }
     for (; t0 + NB <= nt; t0 += NB) {
 #pragma unroll
       for (int d = 0; d < NB; ++d) {
@@ -214,55 +454,37 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     __syncthreads();
     if (trace) trace[5] = globaltimer_ns();  // (re-used) the group is complete
     const int ri = k - (sh.S - R);
-    const int g0 = (int)((long long)sh.RQ * fj / J), g1 = (int)((long long)sh.RQ * (fj + 1) / J);
-    const int r0 = 4 * (g0 + (int)((long long)(g1 - g0) * ri / R));
-    const int r1 = min(sh.m, 4 * (g0 + (int)((long long)(g1 - g0) * (ri + 1) / R)));
-    for (int r = r0 + tid; r < r1; r += kThreads) {
-      float v = 0.f;
-      const float* pp = p.partial + r;
-      for (int ss0 = 0; ss0 < sh.S; ss0 += 16) {  // up to 16 slices per L2 round trip
-        float t[16];
+    const int g0 = group_quad(sh.RQ, J, fj, p.fused_pair), g1 = group_quad(sh.RQ, J, fj + 1, p.fused_pair);
+    if (p.p2p_mode == 0) {
+      // plain output: this reducer's rows of the group, one thread per row
+      const int r0 = 4 * (g0 + (int)((long long)(g1 - g0) * ri / R));
+      const int r1 = min(sh.m, 4 * (g0 + (int)((long long)(g1 - g0) * (ri + 1) / R)));
+      for (int r = r0 + tid; r < r1; r += kThreads) {
+        float v = 0.f;
+        const float* pp = p.partial + r;
+        for (int ss0 = 0; ss0 < sh.S; ss0 += 16) {  // up to 16 slices per L2 round trip
+          float t[16];
 #pragma unroll
-        for (int kk = 0; kk < 16; ++kk) t[kk] = (ss0 + kk < sh.S) ? __ldcg(pp + (size_t)(ss0 + kk) * sh.m4) : 0.f;
+          for (int kk = 0; kk < 16; ++kk) t[kk] = (ss0 + kk < sh.S) ? __ldcg(pp + (size_t)(ss0 + kk) * sh.m4) : 0.f;
 #pragma unroll
-        for (int kk = 0; kk < 16; ++kk)
-          if (ss0 + kk < sh.S) v += t[kk];
-      }
-      if (p.npeers > 0 && p.p2p_f32) {  // fused all-reduce: fp32 partial row into slot `rank` of every rank
-        for (int pr = 0; pr < p.npeers; ++pr) reinterpret_cast<float*>(p.peer_y[pr])[p.yoff + r] = v;
-      } else if (p.npeers > 0) {  // fused rows all-gather (NEXT-1): the row goes to every rank's output over NVLink
-        const __half h = __float2half_rn(v);
-        for (int pr = 0; pr < p.npeers; ++pr) p.peer_y[pr][p.yoff + r] = h;
-      } else if (p.yf) {
-        p.yf[r] = v;
-      } else {
-        p.y[r] = __float2half_rn(v);
-      }
-    }
-    __syncthreads();
-    if (tid == 0 && atomicAdd(depart, 1u) == (unsigned)R - 1) {  // the last reducer resets the pair
-      *arrive = 0u;
-      *depart = 0u;
-    }
-    if (p.npeers > 0 && tid == 0) {
-      // The last reducer of the whole grid signals every rank.  Ordering of every
-      // reducer's peer stores before that signal (PTX memory model, causality order
-      // is transitive across scopes): stores -> bar.sync (CTA) -> this thread's
-      // acq_rel RMW on `done` (gpu scope, both sides on this GPU) -> the last
-      // reducer's acquiring RMW -> its fence.acq_rel.sys -> red.release.sys to the
-      // peer -> the peer's ld.acquire.sys.  A system-scope fence in every reducer
-      // (the first version) is not needed and cost 3.6 us per call.
-      unsigned* done = p.counters + 2 * kFusedMaxJ;
-      if (atom_add_acq_rel_u32(done, 1u) == (unsigned)(J * R) - 1) {
-        *done = 0u;
-        fence_acq_rel_sys();
-        for (int pr = 0; pr < p.npeers; ++pr) red_release_sys_add_u32(p.peer_sig[pr], 1u);
-        // ... and holds the grid open until every rank's rows of this round have
-        // arrived here: the kernel's completion then means "gathered output ready"
-        if (p.p2p_target) {
-          while (ld_acquire_sys_u32(p.peer_sig[p.p2p_self]) < p.p2p_target) __nanosleep(64);
+          for (int kk = 0; kk < 16; ++kk)
+            if (ss0 + kk < sh.S) v += t[kk];
         }
+        if (p.yf) p.yf[r] = v;
+        else p.y[r] = __float2half_rn(v);
       }
+      __syncthreads();
+      if (tid == 0 && atomicAdd(depart, 1u) == (unsigned)R - 1) {  // the last reducer resets the pair
+        *arrive = 0u;
+        *depart = 0u;
+      }
+    } else {
+      __syncthreads();  // every CTA of the group has read its arrival count before the reset below
+      if (tid == 0 && atomicAdd(depart, 1u) == (unsigned)R - 1) {
+        *arrive = 0u;
+        *depart = 0u;
+      }
+      p2p_epilogue(p, J, R, fj, ri, g0, g1);
     }
     if (trace) trace[6] = globaltimer_ns();  // reduction share done
     return;
@@ -341,36 +563,6 @@ cudaError_t launch_reduce(const KParams& p, cudaStream_t st) {
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, lut_reduce_kernel, (const float*)p.partial, p.sh.S, p.b, p.sh.m, p.sh.m4, p.y,
                             p.yf);
-}
-
-// Fused all-reduce, local step: y[r] = sum over ranks pr = 0..P-1 (fixed order,
-// deterministic) of slot[pr][r], fp16 round-to-nearest-even.  Launched with PDL
-// behind the fused GEMV (which triggers its dependents early), so its CTAs are
-// resident and waiting when the GEMV's last reducer has seen the round's signals.
-__global__ void __launch_bounds__(256) p2p_sum_kernel(const float* __restrict__ slots, int P, int m,
-                                                      __half* __restrict__ y) {
-  pdl_wait();
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= m) return;
-  float v = __ldcg(slots + r);
-  for (int pr = 1; pr < P; ++pr) v += __ldcg(slots + (size_t)pr * m + r);
-  y[r] = __float2half_rn(v);
-}
-
-cudaError_t launch_p2p_sum(const float* slots, int P, int m, uint16_t* y, cudaStream_t st) {
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  static bool attr_set = false;
-  if (!attr_set) {  // same carveout as the GEMV: no L1/smem reconfiguration, co-resident while waiting
-    cudaFuncSetAttribute(p2p_sum_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    attr_set = true;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((m + 255) / 256);
-  cfg.blockDim = dim3(256);
-  cfg.stream = st;
-  cfg.attrs = const_cast<cudaLaunchAttribute*>(pdl_attr());
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, p2p_sum_kernel, slots, P, m, reinterpret_cast<__half*>(y));
 }
 
 }  // namespace lg

@@ -25,15 +25,24 @@ struct KParams {
   int qpw;           // batched: row quads per work item (256 or 128)
   int gsh;           // batched: layout lane -> slice-local group shift (31: one group per slice)
   int fused_J;       // GEMV: CTAs per slice in the fused-reduction mode (0: separate reduction kernel)
+  int fused_pair;    // GEMV fused mode: row-quad group boundaries on even quads (8-row units)
+  int smem_pf;       // GEMV fused mode: max row quads per CTA prefetched into shared memory before the PDL wait
+  unsigned l2_pf;    // GEMV fused mode: weight bytes per CTA prefetched into L2 before the PDL wait
   int reducers;      // GEMV fused mode: the last R CTAs to arrive in a row-quad group reduce it
-  // fused rows all-gather (NEXT-1): rank r's output rows go to peer_y[pr] + yoff on every rank pr
-  __half* peer_y[8];
-  unsigned* peer_sig[8];
-  int npeers;        // 0: plain output
+  // fused tensor-parallel epilogue over peer memory (NEXT-1, lutgemm_p2p.cu).  p2p_mode 1 (rows
+  // all-gather): each finished fp16 row r goes to window[par][pr] + p2p_yarea + 2 (yoff + r) of every
+  // rank pr; p2p_mode 2 (column split, reduce-scatter): each fp32 partial row r goes to its owner
+  // o = r / p2p_mb, slot [p2p_self][r - o p2p_mb] of window[par][o].  par = *p2p_round & 1 (device-side
+  // round counter: graph-capturable).  The grid's last reducer then signals every rank (p2p_sig[pr]).
+  uint8_t* p2p_win[2][8];
+  unsigned long long* p2p_sig[8];
+  const unsigned long long* p2p_round;
+  int p2p_mode;      // 0: plain output
+  int npeers;
   int yoff;
-  int p2p_self;      // this rank's index in peer_sig
-  int p2p_f32;       // 1: store fp32 partial rows (fused column-split all-reduce) instead of fp16 rows
-  unsigned p2p_target;  // nonzero: the grid's last reducer waits until peer_sig[p2p_self] >= target
+  int p2p_self;
+  int p2p_mb;
+  unsigned p2p_yarea;
   int s2;            // b <= 4 GEMV-structured kernel: number of sub-slices (0: not used)
   long long items;
   unsigned long long* trace;  // optional per-CTA timeline (kTraceSlots u64 per CTA), or null
@@ -56,14 +65,18 @@ int batch_pad(int b);
 cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, int b, uint16_t* y, float* yf,
                         void* ws, cudaStream_t st);
 
-// NEXT-1: b = 1 product whose fused reduction stores the rows into every rank's
-// output (peer_y[pr] + yoff) and signals every rank (peer_sig[pr]); requires the
-// fused GEMV mode (returns cudaErrorNotSupported otherwise); the grid's last
-// reducer then waits until peer_sig[self] >= target (the round's P signals).
-cudaError_t run_gemv_p2p(const Shape& sh, const void* data, const uint16_t* x, void* ws, __half* const* peer_y,
-                         unsigned* const* peer_sig, int npeers, int yoff, int self, unsigned target, int f32,
-                         cudaStream_t st);
-cudaError_t launch_p2p_sum(const float* slots, int P, int m, uint16_t* y, cudaStream_t st);
+// NEXT-1: b = 1 product whose fused reduction stores the rows into the ranks' windows (see
+// KParams::p2p_*), exchanges with every rank and writes the full result to y; requires the fused
+// GEMV mode (returns cudaErrorNotSupported otherwise).
+struct P2PArgs {
+  uint8_t* win[2][8];
+  unsigned long long* sig[8];
+  const unsigned long long* round;
+  int mode, npeers, self, yoff, mb;
+  unsigned yarea;
+};
+cudaError_t run_gemv_p2p(const Shape& sh, const void* data, const uint16_t* x, void* ws, const P2PArgs& a,
+                         uint16_t* y, cudaStream_t st);
 
 cudaError_t run_pack_bcq(const Shape& sh, const uint32_t* planes, const uint16_t* alpha, const uint16_t* offset,
                          void* dst, cudaStream_t st);

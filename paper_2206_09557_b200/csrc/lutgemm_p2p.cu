@@ -1,48 +1,61 @@
-// lutgemm_p2p.cu -- the rows all-gather of a tensor-parallel GEMV fused into the
-// GEMV's epilogue over peer memory (the paper names the
-// GPU-to-GPU communication as what limits tensor parallelism once the matmul is
-// fast, Table 2).
+// lutgemm_p2p.cu -- the tensor-parallel exchange of a LUT-GEMV fused into the GEMV's epilogue
+// over peer memory (the paper names GPU-to-GPU communication as what limits
+// tensor parallelism once the matmul is fast, Table 2).
 //
-// Every rank owns two output buffers (double buffer) and a signal counter,
-// allocated with cudaMalloc and shared with the other ranks through CUDA IPC
-// handles that the caller exchanges (any transport: the Python binding uses
-// torch.distributed).  A call runs the fused GEMV whose reducer CTAs store each
-// finished row of this rank's shard straight into buffer (round & 1) of every
-// rank (NVLink / NVSwitch P2P stores), then the grid's last reducer signals
-// every rank (red.release.sys) and then holds the grid open until this rank has
-// received the round's P signals (ld.acquire.sys), so the kernel's completion
-// means "gathered output ready" for whatever the stream runs next.  Flow control: a rank
-// writes buffer (k+2) & 1 only after its wait for round k+1, which needs every
-// peer's round-(k+1) signal, sent after that peer's stream ran everything before
-// its round-(k+1) call -- including its consumers of round k.  Contract: the
-// output of a call stays valid until the call after next; calls are made in the
-// same order on every rank.
+// Every rank owns two exchange windows (double buffer) and a 256-byte signal block, allocated
+// with cudaMalloc and shared through CUDA IPC handles that the caller exchanges (any transport;
+// the Python binding uses torch.distributed).  A call is
+// one kernel launch, graph-capturable (no host-side state changes between calls: the round number
+// lives on the device).
+//
+// The whole exchange runs in the fused GEMV's epilogue (lutgemm_gemv.cu, p2p_epilogue), in the
+// reducer CTAs (all resident), 16-byte stores over NVLink / NVSwitch P2P mappings:
+//   rows (m-split, ROWS_ALLGATHER): fp16 rows of this rank's shard -> this rank's y and every
+//     peer's window; signal; wait for the round's P signals; copy the peers' rows window -> y;
+//   cols (n-split, COLS_ALLREDUCE): reduce-scatter + all-gather: fp32 partial rows -> the row's
+//     OWNER rank only (rank o owns rows [o mb, (o+1) mb)), slot [this rank]; signal; wait; the
+//     owner sums its block over the P slots in rank order (deterministic, identical on every
+//     rank), rounds to fp16 and stores it into y and every peer's window; signal; wait; copy the
+//     peers' blocks window -> y.
+// The last reducer advances the device-side round (the parity of the double buffer).
+//
+// Flow control: window (k & 1) is rewritten in round k + 2 only; a rank enters round k + 2 after
+// completing round k + 1, which needs every peer's round-(k+1) signal, sent after that peer's
+// stream completed its round-k GEMV (round k + 1's epilogue starts after its PDL wait).
+// Signal counters are 64-bit (no wrap).  Every rank makes the same sequence of calls.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <new>
 
-#include "layout.cuh"
+#include "kernels_common.cuh"
 #include "lutgemm.h"
-#include "lutgemm_internal.h"
 
 lutgemm_status lutgemm_internal_fail(lutgemm_status st, const char* msg);
+lutgemm_status lutgemm_internal_check_weight(const lutgemm_weight* w);
+lutgemm_status lutgemm_internal_check_device();
+
+// signal block (256 bytes, device): [0] signal A (epilogue stores done), [1] signal B (cols:
+// all-gather stores done), [2] round (local)
+constexpr int kSigA = 0, kRound = 2;
 
 struct lutgemm_p2p {
   int rank, nranks, dev;
-  size_t out_bytes;
-  void* out[2];          // local outputs
-  unsigned* sig;         // local signal counter (256-byte block)
-  void* peer_out[2][8];  // every rank's outputs in this process's address space (self: local)
-  unsigned* peer_sig[8];
+  size_t win_bytes;
+  uint8_t* win[2];                     // local windows
+  unsigned long long* sig;             // local signal block
+  uint8_t* peer_win[2][8];             // every rank's windows in this process's address space (self: local)
+  unsigned long long* peer_sig[8];
   bool connected;
-  unsigned long long round;
 };
 
 namespace {
 
-constexpr int kRec = 256;  // record: 3 IPC handles (64 B each), rank, out_bytes
+using namespace lg;
+
+constexpr int kRec = 256;  // record: 3 IPC handles (64 B each), rank, window bytes
 
 lutgemm_status cuda_fail(cudaError_t e, const char* what) {
   char buf[384];
@@ -50,150 +63,174 @@ lutgemm_status cuda_fail(cudaError_t e, const char* what) {
   return lutgemm_internal_fail(LUTGEMM_ERR_CUDA, buf);
 }
 
+size_t align256(size_t v) { return (v + 255) / 256 * 256; }
+
+// rows owned per rank in the column split (multiple of 8: 16-byte stores, whole 8-row units)
+int block_rows(int m, int P) { return ((m + P - 1) / P + 7) / 8 * 8; }
+
+lutgemm_status run(lutgemm_p2p* g, int mode, const lutgemm_weight* shard, const uint16_t* x, void* ws,
+                   size_t ws_bytes, void* stream, uint16_t* y) {
+  lutgemm_status st = lutgemm_internal_check_weight(shard);  // the shard first: shape errors name the shape
+  if (st != LUTGEMM_OK) return st;
+  if (!g || !g->connected || !x || !ws || !y)
+    return lutgemm_internal_fail(LUTGEMM_ERR_INVALID_ARG, "NULL argument or group not connected");
+  const int P = g->nranks, ms = shard->m;
+  if (mode == 1 && ms % 8)
+    return lutgemm_internal_fail(LUTGEMM_ERR_INVALID_ARG, "rows all-gather needs m_shard % 8 == 0");
+  const int m_out = mode == 1 ? P * ms : ms;
+  const int mb = block_rows(ms, P);
+  const size_t need = lutgemm_p2p_window_bytes(P, mode == 1 ? LUTGEMM_TP_ROWS_ALLGATHER : LUTGEMM_TP_COLS_ALLREDUCE,
+                                               m_out);
+  if (need > g->win_bytes)
+    return lutgemm_internal_fail(LUTGEMM_ERR_INVALID_ARG, "exchange windows too small (lutgemm_p2p_window_bytes)");
+  if (lutgemm_workspace_bytes(shard->m, shard->n, 1) > ws_bytes)
+    return lutgemm_internal_fail(LUTGEMM_ERR_WORKSPACE, "workspace too small");
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(ws) & 15) ||
+      (reinterpret_cast<uintptr_t>(y) & 1))
+    return lutgemm_internal_fail(LUTGEMM_ERR_MISALIGNED, "x and ws must be 16-byte aligned, y 2-byte aligned");
+  st = lutgemm_internal_check_device();
+  if (st != LUTGEMM_OK) return st;
+  const lg::Shape sh = lg::make_shape(shard->m, shard->n, shard->q, shard->g, shard->has_offset,
+                                      shard->format == LUTGEMM_FMT_UNIFORM_COMPACT);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  lg::P2PArgs a;
+  for (int pr = 0; pr < 8; ++pr) {
+    a.win[0][pr] = pr < P ? g->peer_win[0][pr] : nullptr;
+    a.win[1][pr] = pr < P ? g->peer_win[1][pr] : nullptr;
+    a.sig[pr] = pr < P ? g->peer_sig[pr] + kSigA : nullptr;
+  }
+  a.round = g->sig + kRound;
+  a.mode = mode;
+  a.npeers = P;
+  a.self = g->rank;
+  a.yoff = mode == 1 ? g->rank * ms : 0;
+  a.mb = mb;
+  a.yarea = mode == 1 ? 0u : (unsigned)align256((size_t)P * mb * 4);
+  cudaError_t e = lg::run_gemv_p2p(sh, shard->data, x, ws, a, y, s);
+  if (e == cudaErrorNotSupported)
+    return lutgemm_internal_fail(LUTGEMM_ERR_UNSUPPORTED, "shard shape does not run the fused GEMV mode");
+  if (e != cudaSuccess) return cuda_fail(e, "fused GEMV launch");
+  return LUTGEMM_OK;
+}
 }  // namespace
 
 extern "C" {
 
-lutgemm_status lutgemm_p2p_create(int rank, int nranks, size_t out_bytes, lutgemm_p2p** out, uint8_t record[256]) {
+size_t lutgemm_p2p_window_bytes(int nranks, int mode, int m) {
+  if (nranks < 1 || nranks > 8 || m < 1) return 0;
+  if (mode == LUTGEMM_TP_ROWS_ALLGATHER) return align256((size_t)m * 2);
+  if (mode == LUTGEMM_TP_COLS_ALLREDUCE) {
+    const size_t mb = (size_t)block_rows(m, nranks);
+    return align256((size_t)nranks * mb * 4) + align256((size_t)nranks * mb * 2);
+  }
+  return 0;
+}
+
+lutgemm_status lutgemm_p2p_create(int rank, int nranks, size_t win_bytes, lutgemm_p2p** out, uint8_t record[256]) {
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
-  if (!out || !record || nranks < 1 || nranks > 8 || rank < 0 || rank >= nranks || out_bytes == 0)
+  if (!out || !record || nranks < 1 || nranks > 8 || rank < 0 || rank >= nranks || win_bytes == 0)
     return lutgemm_internal_fail(LUTGEMM_ERR_INVALID_ARG, "bad p2p_create arguments (1 <= nranks <= 8)");
   lutgemm_p2p* g = new (std::nothrow) lutgemm_p2p;
   if (!g) return lutgemm_internal_fail(LUTGEMM_ERR_INVALID_ARG, "out of host memory");
   memset(g, 0, sizeof(*g));
   g->rank = rank;
   g->nranks = nranks;
-  g->out_bytes = (out_bytes + 255) / 256 * 256;
+  g->win_bytes = align256(win_bytes);
   cudaGetDevice(&g->dev);
-  cudaError_t e = cudaMalloc(&g->out[0], g->out_bytes);
-  if (e == cudaSuccess) e = cudaMalloc(&g->out[1], g->out_bytes);
+  cudaError_t e = cudaMalloc(&g->win[0], g->win_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&g->win[1], g->win_bytes);
   if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&g->sig), 256);
   if (e == cudaSuccess) e = cudaMemset(g->sig, 0, 256);
+  if (e == cudaSuccess) e = cudaMemset(g->win[0], 0, g->win_bytes);
+  if (e == cudaSuccess) e = cudaMemset(g->win[1], 0, g->win_bytes);
   memset(record, 0, kRec);
   cudaIpcMemHandle_t h[3];
-  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h[0], g->out[0]);
-  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h[1], g->out[1]);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h[0], g->win[0]);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h[1], g->win[1]);
   if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h[2], g->sig);
   if (e != cudaSuccess) {
     lutgemm_p2p_destroy(g);
-    return cuda_fail(e, "p2p buffers / IPC handles");
+    return cuda_fail(e, "p2p windows / IPC handles");
   }
   memcpy(record, h, 3 * 64);
   memcpy(record + 192, &rank, sizeof(int));
-  const unsigned long long ob = g->out_bytes;
-  memcpy(record + 200, &ob, sizeof(ob));
+  const unsigned long long wb = g->win_bytes;
+  memcpy(record + 200, &wb, sizeof(wb));
   *out = g;
   return LUTGEMM_OK;
 }
 
 lutgemm_status lutgemm_p2p_connect(lutgemm_p2p* g, const uint8_t* records) {
   if (!g || !records) return lutgemm_internal_fail(LUTGEMM_ERR_INVALID_ARG, "NULL argument");
+  if (g->connected) return lutgemm_internal_fail(LUTGEMM_ERR_INVALID_ARG, "group already connected");
   for (int pr = 0; pr < g->nranks; ++pr) {
-    const uint8_t* rec = records + (size_t)pr * kRec;
     int r;
-    unsigned long long ob;
-    memcpy(&r, rec + 192, sizeof(int));
-    memcpy(&ob, rec + 200, sizeof(ob));
-    if (r != pr || ob != g->out_bytes)
-      return lutgemm_internal_fail(LUTGEMM_ERR_INVALID_ARG, "records must be in rank order with equal out_bytes");
+    unsigned long long wb;
+    memcpy(&r, records + (size_t)pr * kRec + 192, sizeof(int));
+    memcpy(&wb, records + (size_t)pr * kRec + 200, sizeof(wb));
+    if (r != pr || wb != g->win_bytes)
+      return lutgemm_internal_fail(LUTGEMM_ERR_INVALID_ARG, "records must be in rank order with equal window sizes");
+  }
+  for (int pr = 0; pr < g->nranks; ++pr) {
     if (pr == g->rank) {
-      g->peer_out[0][pr] = g->out[0];
-      g->peer_out[1][pr] = g->out[1];
+      g->peer_win[0][pr] = g->win[0];
+      g->peer_win[1][pr] = g->win[1];
       g->peer_sig[pr] = g->sig;
       continue;
     }
     cudaIpcMemHandle_t h[3];
-    memcpy(h, rec, 3 * 64);
+    memcpy(h, records + (size_t)pr * kRec, 3 * 64);
     void* p[3] = {nullptr, nullptr, nullptr};
     for (int i = 0; i < 3; ++i) {
       cudaError_t e = cudaIpcOpenMemHandle(&p[i], h[i], cudaIpcMemLazyEnablePeerAccess);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+      if (e != cudaSuccess) {
+        // close what this call opened (this peer's and every earlier peer's mappings)
+        for (int j = 0; j < i; ++j) cudaIpcCloseMemHandle(p[j]);
+        for (int q = 0; q < pr; ++q) {
+          if (q == g->rank) continue;
+          cudaIpcCloseMemHandle(g->peer_win[0][q]);
+          cudaIpcCloseMemHandle(g->peer_win[1][q]);
+          cudaIpcCloseMemHandle(g->peer_sig[q]);
+          g->peer_win[0][q] = g->peer_win[1][q] = nullptr;
+          g->peer_sig[q] = nullptr;
+        }
+        return cuda_fail(e, "cudaIpcOpenMemHandle");
+      }
     }
-    g->peer_out[0][pr] = p[0];
-    g->peer_out[1][pr] = p[1];
-    g->peer_sig[pr] = static_cast<unsigned*>(p[2]);
+    g->peer_win[0][pr] = static_cast<uint8_t*>(p[0]);
+    g->peer_win[1][pr] = static_cast<uint8_t*>(p[1]);
+    g->peer_sig[pr] = static_cast<unsigned long long*>(p[2]);
   }
   g->connected = true;
   return LUTGEMM_OK;
 }
 
 lutgemm_status lutgemm_p2p_gemv_allgather(lutgemm_p2p* g, const lutgemm_weight* shard, const uint16_t* x, void* ws,
-                                          size_t ws_bytes, void* stream, uint16_t** y_full, uint16_t* y_copy) {
-  if (!g || !g->connected || !shard || !shard->data || !x || !ws)
-    return lutgemm_internal_fail(LUTGEMM_ERR_INVALID_ARG, "NULL argument or group not connected");
-  const size_t m_total = (size_t)g->nranks * shard->m;
-  if (m_total * 2 > g->out_bytes)
-    return lutgemm_internal_fail(LUTGEMM_ERR_INVALID_ARG, "output buffers too small for nranks * m_shard rows");
-  if (lutgemm_workspace_bytes(shard->m, shard->n, 1) > ws_bytes)
-    return lutgemm_internal_fail(LUTGEMM_ERR_WORKSPACE, "workspace too small");
-  if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(ws) & 15) ||
-      (reinterpret_cast<uintptr_t>(shard->data) & 15))
-    return lutgemm_internal_fail(LUTGEMM_ERR_MISALIGNED, "x, ws and the weight must be 16-byte aligned");
-  const lg::Shape sh = lg::make_shape(shard->m, shard->n, shard->q, shard->g, shard->has_offset,
-                                      shard->format == LUTGEMM_FMT_UNIFORM_COMPACT);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int parity = (int)(g->round & 1);
-  __half* peer_y[8];
-  for (int pr = 0; pr < g->nranks; ++pr) peer_y[pr] = static_cast<__half*>(g->peer_out[parity][pr]);
-  // the grid's last reducer waits for the round's P signals itself (no wait kernel)
-  const unsigned target = (unsigned)((g->round + 1) * g->nranks);
-  cudaError_t e = lg::run_gemv_p2p(sh, shard->data, x, ws, peer_y, g->peer_sig, g->nranks, g->rank * shard->m,
-                                   g->rank, target, 0, st);
-  if (e == cudaErrorNotSupported)
-    return lutgemm_internal_fail(LUTGEMM_ERR_UNSUPPORTED, "shard shape does not run the fused GEMV mode");
-  if (e != cudaSuccess) return cuda_fail(e, "fused GEMV launch");
-  g->round += 1;
-  if (y_copy) {
-    e = cudaMemcpyAsync(y_copy, g->out[parity], m_total * 2, cudaMemcpyDeviceToDevice, st);
-    if (e != cudaSuccess) return cuda_fail(e, "output copy");
-  }
-  if (y_full) *y_full = static_cast<uint16_t*>(g->out[parity]);
-  return LUTGEMM_OK;
+                                          size_t ws_bytes, void* stream, uint16_t* y) {
+  return run(g, 1, shard, x, ws, ws_bytes, stream, y);
 }
 
 lutgemm_status lutgemm_p2p_gemv_allreduce(lutgemm_p2p* g, const lutgemm_weight* shard, const uint16_t* x, void* ws,
                                           size_t ws_bytes, void* stream, uint16_t* y) {
-  if (!g || !g->connected || !shard || !shard->data || !x || !ws || !y)
-    return lutgemm_internal_fail(LUTGEMM_ERR_INVALID_ARG, "NULL argument or group not connected");
-  const size_t m = (size_t)shard->m;
-  if ((size_t)g->nranks * m * 4 > g->out_bytes)
-    return lutgemm_internal_fail(LUTGEMM_ERR_INVALID_ARG, "buffers too small for nranks * m fp32 partial rows");
-  if (lutgemm_workspace_bytes(shard->m, shard->n, 1) > ws_bytes)
-    return lutgemm_internal_fail(LUTGEMM_ERR_WORKSPACE, "workspace too small");
-  if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(ws) & 15) ||
-      (reinterpret_cast<uintptr_t>(shard->data) & 15) || (reinterpret_cast<uintptr_t>(y) & 1))
-    return lutgemm_internal_fail(LUTGEMM_ERR_MISALIGNED, "x, ws and the weight must be 16-byte aligned");
-  const lg::Shape sh = lg::make_shape(shard->m, shard->n, shard->q, shard->g, shard->has_offset,
-                                      shard->format == LUTGEMM_FMT_UNIFORM_COMPACT);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int parity = (int)(g->round & 1);
-  __half* peer_y[8];
-  for (int pr = 0; pr < g->nranks; ++pr) peer_y[pr] = static_cast<__half*>(g->peer_out[parity][pr]);
-  const unsigned target = (unsigned)((g->round + 1) * g->nranks);
-  // fp32 partial row r of this rank -> slot [rank][r] of every rank
-  cudaError_t e = lg::run_gemv_p2p(sh, shard->data, x, ws, peer_y, g->peer_sig, g->nranks,
-                                   (int)(g->rank * m), g->rank, target, 1, st);
-  if (e == cudaErrorNotSupported)
-    return lutgemm_internal_fail(LUTGEMM_ERR_UNSUPPORTED, "shard shape does not run the fused GEMV mode");
-  if (e != cudaSuccess) return cuda_fail(e, "fused GEMV launch");
-  g->round += 1;
-  e = lg::launch_p2p_sum(static_cast<const float*>(g->out[parity]), g->nranks, (int)m, y, st);
-  if (e != cudaSuccess) return cuda_fail(e, "p2p sum launch");
-  return LUTGEMM_OK;
+  return run(g, 2, shard, x, ws, ws_bytes, stream, y);
 }
 
 lutgemm_status lutgemm_p2p_destroy(lutgemm_p2p* g) {
   if (!g) return LUTGEMM_OK;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(g->dev);
   cudaDeviceSynchronize();
   for (int pr = 0; pr < g->nranks; ++pr) {
-    if (pr == g->rank || !g->connected) continue;
-    if (g->peer_out[0][pr]) cudaIpcCloseMemHandle(g->peer_out[0][pr]);
-    if (g->peer_out[1][pr]) cudaIpcCloseMemHandle(g->peer_out[1][pr]);
+    if (pr == g->rank) continue;
+    if (g->peer_win[0][pr]) cudaIpcCloseMemHandle(g->peer_win[0][pr]);
+    if (g->peer_win[1][pr]) cudaIpcCloseMemHandle(g->peer_win[1][pr]);
     if (g->peer_sig[pr]) cudaIpcCloseMemHandle(g->peer_sig[pr]);
   }
-  if (g->out[0]) cudaFree(g->out[0]);
-  if (g->out[1]) cudaFree(g->out[1]);
+  if (g->win[0]) cudaFree(g->win[0]);
+  if (g->win[1]) cudaFree(g->win[1]);
   if (g->sig) cudaFree(g->sig);
+  cudaSetDevice(cur);
   delete g;
   return LUTGEMM_OK;
 }

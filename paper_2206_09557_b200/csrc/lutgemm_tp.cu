@@ -85,6 +85,23 @@ lutgemm_status lutgemm_tp_init(int nranks, int rank, const uint8_t id[128], lutg
   return LUTGEMM_OK;
 }
 
+lutgemm_status lutgemm_tp_async_error(lutgemm_tp* tp) {
+  if (!tp) return lutgemm_internal_fail(LUTGEMM_ERR_INVALID_ARG, "tp is NULL");
+  ncclResult_t async = ncclSuccess;
+  ncclResult_t r = ncclCommGetAsyncError(tp->comm, &async);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclCommGetAsyncError");
+  if (async != ncclSuccess && async != ncclInProgress) return nccl_fail(async, "NCCL asynchronous error");
+  return LUTGEMM_OK;
+}
+
+lutgemm_status lutgemm_tp_abort(lutgemm_tp* tp) {
+  if (!tp) return LUTGEMM_OK;
+  ncclResult_t r = ncclCommAbort(tp->comm);
+  delete tp;
+  if (r != ncclSuccess) return nccl_fail(r, "ncclCommAbort");
+  return LUTGEMM_OK;
+}
+
 int lutgemm_tp_rank(const lutgemm_tp* tp) { return tp ? tp->rank : -1; }
 int lutgemm_tp_nranks(const lutgemm_tp* tp) { return tp ? tp->nranks : -1; }
 

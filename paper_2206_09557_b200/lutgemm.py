@@ -63,9 +63,10 @@ SIGNATURES = [
     ("lutgemm_trace_enable", _I, [_I]),
     ("lutgemm_trace_read", _SZ, [ctypes.POINTER(ctypes.c_uint64), _SZ]),
     ("lutgemm_launch_count", ctypes.c_uint64, []),
+    ("lutgemm_p2p_window_bytes", _SZ, [_I, _I, _I]),
     ("lutgemm_p2p_create", _I, [_I, _I, _SZ, ctypes.POINTER(_P), _P]),
     ("lutgemm_p2p_connect", _I, [_P, _P]),
-    ("lutgemm_p2p_gemv_allgather", _I, [_P, ctypes.POINTER(lutgemm_weight), _P, _P, _SZ, _P, ctypes.POINTER(_P), _P]),
+    ("lutgemm_p2p_gemv_allgather", _I, [_P, ctypes.POINTER(lutgemm_weight), _P, _P, _SZ, _P, _P]),
     ("lutgemm_p2p_gemv_allreduce", _I, [_P, ctypes.POINTER(lutgemm_weight), _P, _P, _SZ, _P, _P]),
     ("lutgemm_p2p_destroy", _I, [_P]),
     ("lutgemm_quantize_rtn", _I, [_P, _I, _I, _I, _I, _P, _P, _P, _P]),
@@ -75,6 +76,8 @@ SIGNATURES = [
     ("lutgemm_tp_workspace_bytes", _SZ, [_P, _I, _I, _I, _I]),
     ("lutgemm_tp_linear", _I, [_P, _I, ctypes.POINTER(lutgemm_weight), _P, _I, _P, _P, _SZ, _P]),
     ("lutgemm_tp_destroy", _I, [_P]),
+    ("lutgemm_tp_async_error", _I, [_P]),
+    ("lutgemm_tp_abort", _I, [_P]),
     ("lutgemm_tp_rank", _I, [_P]),
     ("lutgemm_tp_nranks", _I, [_P]),
 ]
@@ -288,6 +291,33 @@ class TPComm:
                                                           _stream(stream)))
         return y
 
+    def check(self):
+        """Raise LutgemmError if the communicator hit an asynchronous NCCL error."""
+        _check("lutgemm_tp_async_error", lib.lutgemm_tp_async_error(self.handle))
+
+    def wait(self, stream=None, timeout_s: float = 300.0, poll_s: float = 0.001):
+        """Wait for `stream` while polling the communicator for asynchronous errors (failure
+        detection): on an NCCL error or after timeout_s the communicator is aborted (which
+        releases kernels stuck in its collectives) and LutgemmError / TimeoutError is raised."""
+        import time
+        s = torch.cuda.current_stream() if stream is None else stream
+        t0 = time.monotonic()
+        while not s.query():
+            st = lib.lutgemm_tp_async_error(self.handle)
+            if st != OK:
+                msg = lib.lutgemm_last_error().decode(errors="replace")
+                self.abort()
+                raise LutgemmError("lutgemm_tp_async_error", st, msg)
+            if time.monotonic() - t0 > timeout_s:
+                self.abort()
+                raise TimeoutError(f"stream not done after {timeout_s} s; NCCL communicator aborted")
+            time.sleep(poll_s)
+
+    def abort(self):
+        if self.handle:
+            lib.lutgemm_tp_abort(self.handle)
+            self.handle = None
+
     def close(self):
         if self.handle:
             _check("lutgemm_tp_destroy", lib.lutgemm_tp_destroy(self.handle))
@@ -325,39 +355,53 @@ def lutgemm_quantize_bcq(W: torch.Tensor, q: int, g: int, iters: int = 0, stream
     return planes, alpha
 
 
-class P2PGroup:
-    """Fused GEMV + rows all-gather over peer memory (lutgemm_p2p_*).
-    The 256-byte IPC records travel over the caller's torch.distributed group
-    (plumbing only; gloo or nccl); one process per GPU (or, for testing, per
-    process on one GPU)."""
+def lutgemm_p2p_window_bytes(world: int, mode: int, m: int) -> int:
+    """Bytes of one exchange window: mode TP_ROWS_ALLGATHER (m = gathered rows) or TP_COLS_ALLREDUCE (m = rows)."""
+    return int(lib.lutgemm_p2p_window_bytes(world, mode, m))
 
-    def __init__(self, rank: int, world: int, out_elems: int, group=None, out_bytes: int | None = None):
+
+class P2PGroup:
+    """Tensor-parallel exchange fused into the GEMV over peer memory (lutgemm_p2p_*):
+    rows all-gather and column reduce-scatter + all-gather.  The 256-byte IPC records travel over the
+    caller's torch.distributed group (plumbing only; gloo or nccl); one process per GPU (or, for
+    testing, per process on one GPU).  Calls are CUDA-graph capturable.  ``rows_out`` / ``cols_m``
+    size the windows for the largest gathered output / column-split layer the group will serve."""
+
+    def __init__(self, rank: int, world: int, rows_out: int = 0, cols_m: int = 0, group=None):
         import torch.distributed as dist
+        nbytes = max(lutgemm_p2p_window_bytes(world, TP_ROWS_ALLGATHER, rows_out) if rows_out else 0,
+                     lutgemm_p2p_window_bytes(world, TP_COLS_ALLREDUCE, cols_m) if cols_m else 0)
+        if nbytes <= 0:
+            raise ValueError("P2PGroup needs rows_out > 0 or cols_m > 0")
         rec = (ctypes.c_uint8 * 256)()
         h = _P()
-        nbytes = out_bytes if out_bytes is not None else 2 * out_elems
         _check("lutgemm_p2p_create", lib.lutgemm_p2p_create(rank, world, nbytes, ctypes.byref(h),
                                                             ctypes.cast(rec, _P)))
         self.handle, self.rank, self.world = h, rank, world
-        if world > 1:
-            recs = [None] * world
-            dist.all_gather_object(recs, bytes(rec), group=group)
-        else:
-            recs = [bytes(rec)]
-        allrec = (ctypes.c_uint8 * (256 * world)).from_buffer_copy(b"".join(recs))
-        _check("lutgemm_p2p_connect", lib.lutgemm_p2p_connect(self.handle, ctypes.cast(allrec, _P)))
+        try:
+            if world > 1:
+                recs = [None] * world
+                dist.all_gather_object(recs, bytes(rec), group=group)
+            else:
+                recs = [bytes(rec)]
+            allrec = (ctypes.c_uint8 * (256 * world)).from_buffer_copy(b"".join(recs))
+            _check("lutgemm_p2p_connect", lib.lutgemm_p2p_connect(self.handle, ctypes.cast(allrec, _P)))
+        except BaseException:
+            lib.lutgemm_p2p_destroy(self.handle)
+            self.handle = None
+            raise
 
-    def gemv_allgather(self, shard: PackedBCQ, x: torch.Tensor, ws: torch.Tensor, y: torch.Tensor | None = None,
-                       stream=None) -> torch.Tensor | None:
-        """Run one fused call; if y (CUDA fp16 [world * m_shard]) is given, the gathered result is copied there."""
+    def gemv_allgather(self, shard: PackedBCQ, x: torch.Tensor, ws: torch.Tensor, y: torch.Tensor,
+                       stream=None) -> torch.Tensor:
+        """Rows split: y (CUDA fp16 [world * m_shard]) = every rank's shard rows times x."""
         _check("lutgemm_p2p_gemv_allgather",
                lib.lutgemm_p2p_gemv_allgather(self.handle, ctypes.byref(shard.struct), x.data_ptr(), ws.data_ptr(),
-                                              ws.numel(), _stream(stream), None, _ptr(y)))
+                                              ws.numel(), _stream(stream), y.data_ptr()))
         return y
 
     def gemv_allreduce(self, shard: PackedBCQ, x_local: torch.Tensor, ws: torch.Tensor, y: torch.Tensor,
                        stream=None) -> torch.Tensor:
-        """Column split: y [m] fp16 = sum over ranks of shard_r x_r (fused fp32 partial exchange)."""
+        """Column split: y [m] fp16 = sum over ranks of shard_r x_r (fused reduce-scatter + all-gather)."""
         _check("lutgemm_p2p_gemv_allreduce",
                lib.lutgemm_p2p_gemv_allreduce(self.handle, ctypes.byref(shard.struct), x_local.data_ptr(),
                                               ws.data_ptr(), ws.numel(), _stream(stream), y.data_ptr()))

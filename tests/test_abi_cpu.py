@@ -95,6 +95,18 @@ def test_p2p_argument_validation_without_gpu():
     assert lib.lutgemm_p2p_create(0, 1, 0, ctypes.byref(h), rec) == 1   # out_bytes 0
     assert lib.lutgemm_p2p_connect(None, rec) == 1
     w = B.lutgemm_weight()
-    assert lib.lutgemm_p2p_gemv_allgather(None, ctypes.byref(w), None, None, 0, None, None, None) == 1
+    assert lib.lutgemm_p2p_gemv_allgather(None, ctypes.byref(w), None, None, 0, None, None) == 1
     assert lib.lutgemm_p2p_gemv_allreduce(None, ctypes.byref(w), None, None, 0, None, None) == 1
     assert lib.lutgemm_p2p_destroy(None) == 0
+    # the shard is validated like any weight (shape rule, format, alignment) before the group
+    for bad, msg in [((64, 1024, 9, 128, 0, 0, 4096), b"q=9"), ((64, 1024, 3, 96, 0, 0, 4096), b"g=96"),
+                     ((64, 1024, 3, 128, 0, 7, 4096), b"format"), ((64, 1024, 3, 128, 0, 0, 4100), b"aligned")]:
+        w = B.lutgemm_weight(*bad)
+        for fn in (lib.lutgemm_p2p_gemv_allgather, lib.lutgemm_p2p_gemv_allreduce):
+            st = fn(None, ctypes.byref(w), 4096, 8192, 1 << 20, None, 16384)
+            assert st in (1, 2) and msg in lib.lutgemm_last_error(), (bad, lib.lutgemm_last_error())
+    # window sizes: rows = 2 m (256-B rounded); cols = P mb fp32 slots + P mb fp16, mb = 8 ceil(ceil(m/P)/8)
+    assert lib.lutgemm_p2p_window_bytes(8, B.TP_ROWS_ALLGATHER, 49152) == 98304
+    assert lib.lutgemm_p2p_window_bytes(8, B.TP_COLS_ALLREDUCE, 12288) == 8 * 1536 * 4 + 8 * 1536 * 2
+    assert lib.lutgemm_p2p_window_bytes(3, B.TP_COLS_ALLREDUCE, 100) == 512 + 256  # mb = 40: 480 B + 240 B, 256-B rounded
+    assert lib.lutgemm_p2p_window_bytes(9, B.TP_COLS_ALLREDUCE, 100) == 0

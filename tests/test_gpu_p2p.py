@@ -25,7 +25,7 @@ def test_p2p_world1_matches_gemv():
     d = gen_bcq(3, m, n, q, g)
     w = L.lutgemm_pack_bcq(torch.from_numpy(d["planes"].view(np.int32)).cuda(), torch.from_numpy(d["alpha"]).cuda(),
                            None, n, g)
-    grp = L.P2PGroup(0, 1, m)
+    grp = L.P2PGroup(0, 1, rows_out=m)
     ws = L.make_workspace(L.lutgemm_workspace_bytes(m, n, 1), "cuda")
     for r in range(5):
         x = torch.from_numpy(gen_x(r, 1, n)[0]).cuda()
@@ -45,7 +45,7 @@ def test_p2p_allreduce_world1_matches_gemv():
     d = gen_bcq(5, m, n, q, g)
     w = L.lutgemm_pack_bcq(torch.from_numpy(d["planes"].view(np.int32)).cuda(), torch.from_numpy(d["alpha"]).cuda(),
                            None, n, g)
-    grp = L.P2PGroup(0, 1, m, out_bytes=4 * m)
+    grp = L.P2PGroup(0, 1, rows_out=m, cols_m=m)
     ws = L.make_workspace(L.lutgemm_workspace_bytes(m, n, 1), "cuda")
     for r in range(5):
         x = torch.from_numpy(gen_x(r, 1, n)[0]).cuda()
@@ -68,7 +68,7 @@ def test_p2p_world1_uniform_offset_formats(mode, compact):
     u = gen_uniform(6, m, n, q, g)
     w = L.lutgemm_pack_uniform(torch.from_numpy(u["codes"]).cuda(), torch.from_numpy(u["scale"]).cuda(),
                                torch.from_numpy(u["zero"]).cuda(), q, g, compact=compact)
-    grp = L.P2PGroup(0, 1, m, out_bytes=4 * m)
+    grp = L.P2PGroup(0, 1, rows_out=m, cols_m=m)
     ws = L.make_workspace(L.lutgemm_workspace_bytes(m, n, 1), "cuda")
     planes, alpha, z = O.uniform_to_bcq(u["codes"], u["scale"], u["zero"], q)
     for r in range(3):
@@ -92,31 +92,41 @@ def test_p2p_rejects_unfused_shapes():
     d = gen_bcq(4, 8, 1024, 3, 128)  # 2 row quads < J CTAs per slice: not the fused mode
     w = L.lutgemm_pack_bcq(torch.from_numpy(d["planes"].view(np.int32)).cuda(), torch.from_numpy(d["alpha"]).cuda(),
                            None, 1024, 128)
-    grp = L.P2PGroup(0, 1, 8)
+    grp = L.P2PGroup(0, 1, rows_out=8)
     ws = L.make_workspace(L.lutgemm_workspace_bytes(8, 1024, 1), "cuda")
     with pytest.raises(L.LutgemmError) as ei:
-        grp.gemv_allgather(w, torch.zeros(1024, dtype=torch.float16, device="cuda"), ws)
+        grp.gemv_allgather(w, torch.zeros(1024, dtype=torch.float16, device="cuda"), ws,
+                           torch.empty(8, dtype=torch.float16, device="cuda"))
     assert ei.value.status == 6
     grp.close()
 
 
-@pytest.mark.parametrize("nproc", [2, 4])
-def test_p2p_multi_process_same_gpu(nproc):
+def _run_check(nproc, port, *args):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29540 + nproc),
-           os.path.join(ROOT, "tools", "p2p_check.py"), "--same-device", "--rounds", "4"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(ROOT, "tools", "p2p_check.py"), "--same-device", *args]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
-    assert out.count("bitwise: True") == 4 * nproc and "bitwise: False" not in out
+    return out
 
 
+@pytest.mark.parametrize("graph", [False, True])
+@pytest.mark.parametrize("mode", ["rows", "cols"])
 @pytest.mark.parametrize("nproc", [2, 4])
-def test_p2p_allreduce_multi_process_same_gpu(nproc):
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29550 + nproc),
-           os.path.join(ROOT, "tools", "p2p_check.py"), "--same-device", "--rounds", "4", "--mode", "cols"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
-    out = r.stdout + r.stderr
-    assert r.returncode == 0, out[-4000:]
-    assert out.count(": PASS") == 4 * nproc and ": FAIL" not in out
+def test_p2p_multi_process_same_gpu(nproc, mode, graph):
+    """nproc processes share the GPU through CUDA IPC; 4 rounds issued back to back without a host
+    synchronisation (or captured in a CUDA graph and replayed twice); every rank's result of every
+    round against the fp64 oracle, plus bitwise checks (rows: == 1-GPU GEMV; cols: equal across ranks)."""
+    port = 29540 + nproc + (10 if mode == "cols" else 0) + (20 if graph else 0)
+    out = _run_check(nproc, port, "--rounds", "4", "--mode", mode, *(["--graph"] if graph else []))
+    assert out.count(": PASS") == 4 * nproc and ": FAIL" not in out, out[-3000:]
+
+
+def test_p2p_world1_graph_capture():
+    """World 1, both modes: a CUDA graph of rounds replays correctly (device-side round counter)."""
+    for mode in ("rows", "cols"):
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "p2p_check.py"), "--rounds", "5", "--graph",
+                            "--mode", mode], capture_output=True, text=True, timeout=600, cwd=ROOT)
+        out = r.stdout + r.stderr
+        assert r.returncode == 0 and out.count(": PASS") == 5, out[-3000:]

@@ -61,7 +61,7 @@ def main():
     m, n = 6000, 4096
     d = gen_bcq(9, m, n, 3, 128)
     w = L.lutgemm_pack_bcq(dev(d["planes"].view(np.int32)), dev(d["alpha"]), None, n, 128)
-    grp = L.P2PGroup(0, 1, m)
+    grp = L.P2PGroup(0, 1, rows_out=m)
     ws = L.make_workspace(L.lutgemm_workspace_bytes(m, n, 1), "cuda")
     for r in range(3):
         x = dev(gen_x(r, 1, n)[0])
@@ -71,7 +71,7 @@ def main():
         torch.cuda.synchronize()
         assert torch.equal(y.view(torch.int16), ref.view(torch.int16))
     grp.close()
-    grp = L.P2PGroup(0, 1, m, out_bytes=4 * m)  # fused column all-reduce (fp32 slots + P-way sum)
+    grp = L.P2PGroup(0, 1, cols_m=m)  # fused column reduce-scatter + all-gather
     for r in range(3):
         x = dev(gen_x(r, 1, n)[0])
         y = torch.empty(m, dtype=torch.float16, device="cuda")

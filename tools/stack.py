@@ -2,20 +2,25 @@
 {QKV 36864x12288, out 12288x12288, fc1 49152x12288, fc2 12288x49152}, q=3,
 g=128), one token (b=1), per-token latency on 1 GPU or tensor-parallel.
 
-    python tools/stack.py [--layers 96] [--tokens 20] [--check]
-    torchrun --nproc-per-node P tools/stack.py ...
+    python tools/stack.py [--layers 96] [--tokens 20] [--check] [--tp-impl nccl|p2p]
+    torchrun --nproc-per-node P tools/stack.py [--tp-impl p2p [--same-device]] ...
 
 Tensor parallelism (Megatron pairing): QKV and fc1 are split by
 rows (no communication), out-proj and fc2 by columns -- each rank's input is
 its own QKV / fc1 output slice -- followed by an fp32 all-reduce of y
-(lutgemm_tp_linear COLS_ALLREDUCE): 2 all-reduces per layer.  Attention, LN
+(lutgemm_tp_linear COLS_ALLREDUCE with NCCL, or --tp-impl p2p: the reduce-scatter + all-gather
+fused into the GEMV epilogue over peer memory, lutgemm_p2p_gemv_allreduce): 2 all-reduces per layer.
+--same-device (p2p only) runs every rank on cuda:0 through CUDA IPC: the single-GPU validation of the
+multi-rank path (NCCL refuses two ranks on one GPU).  Attention, LN
 and embeddings are omitted (the path is the linears): out-proj reads the first
 12288/P outputs of QKV.  Weights are seeded synthetic BCQ (device RNG), 73.4 GB
 at P=1.  One token = one CUDA graph of 384 LUT-GEMMs (+ 192 all-reduces).
 
 --check: for layers 0 and L-1 each linear is also run on a seeded x and 64
 sampled rows are compared with the fp64 oracle (its inputs are the seeded
-canonical weights copied to the host before packing, never a CUDA output).
+canonical weights copied to the host before packing, never a CUDA output);
+the column-split linears through the actual TP exchange (the oracle partials of
+every rank's shard summed across ranks).
 """
 from __future__ import annotations
 
@@ -55,18 +60,25 @@ def main():
     ap.add_argument("--tokens", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--check", action="store_true")
+    ap.add_argument("--tp-impl", default="nccl", choices=["nccl", "p2p"])
+    ap.add_argument("--same-device", action="store_true")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    comm = None
+    dev = torch.device("cuda", 0 if args.same_device else local)
+    torch.cuda.set_device(dev)
+    comm = p2p = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-        comm = L.TPComm(rank, world, device=dev)
+        if args.tp_impl == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+            comm = L.TPComm(rank, world, device=dev)
+        else:
+            dist.init_process_group("gloo")
+    if args.tp_impl == "p2p":
+        p2p = L.P2PGroup(rank, world, cols_m=H)
 
     t0 = time.time()
     weights = []  # per layer: dict name -> PackedBCQ
@@ -105,7 +117,9 @@ def main():
                                    comm.workspace_bytes(L.TP_COLS_ALLREDUCE, H, 4 * H // world, 1)), dev)
 
     def cols(w, xin, y):
-        if comm is None:
+        if p2p is not None:
+            p2p.gemv_allreduce(w, xin, ws, y)
+        elif comm is None:
             L.lutgemm_gemv(w, xin, y, ws)
         else:
             comm.linear(L.TP_COLS_ALLREDUCE, w, xin, y, tws)
@@ -128,8 +142,8 @@ def main():
     for _ in range(args.warmup):
         graph.replay()
     torch.cuda.synchronize()
-    if comm is not None:
-        torch.distributed.barrier(device_ids=[local])
+    if world > 1:
+        torch.distributed.barrier()
     a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(args.tokens):
@@ -137,8 +151,8 @@ def main():
     e.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(e) / args.tokens
-    if comm is not None:
-        t = torch.tensor([ms], device=dev)
+    if world > 1:
+        t = torch.tensor([ms], device=dev if comm is not None else "cpu")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t[0])
     finite = bool(torch.isfinite(x.float()).all())
@@ -172,21 +186,38 @@ def main():
             got = y.float().cpu().numpy()[rows].astype(np.float64)
             ref = O.bcq_gemv(planes_rows, alpha_rows, None, xs[None], ns_, G)[0]
             parity[f"L{layer}.{name}"] = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+            if name in ("out", "fc2") and (world > 1 or p2p is not None):
+                # the TP output of the column split: sum over ranks of each shard's oracle partial
+                xf = np.random.default_rng(layer * 7 + len(name) + 1).standard_normal(ns_ * world).astype(np.float16)
+                xl = xf[rank * ns_:(rank + 1) * ns_]
+                cols(weights[layer][name], torch.from_numpy(xl).to(dev), y)
+                torch.cuda.synchronize()
+                part = O.bcq_gemv(planes_rows, alpha_rows, None, xl[None], ns_, G)[0]
+                if world > 1:
+                    t = torch.from_numpy(part).to(dev if comm is not None else "cpu")
+                    torch.distributed.all_reduce(t)
+                    part = t.cpu().numpy()
+                got = y.float().cpu().numpy()[rows].astype(np.float64)
+                parity[f"L{layer}.{name}.tp"] = float(np.linalg.norm(got - part) / np.linalg.norm(part))
 
     bytes_token = sum(((m // world) * n if s == "rows" else m * (n // world)) * (Q / 8 + 2 * Q / G)
                       for _, m, n, s in LINEARS) * args.layers
     if rank == 0:
         print(json.dumps({
             "config": "OPT-175B decoder linear stack (96 x QKV/out/fc1/fc2), q=3 g=128, b=1",
-            "layers": args.layers, "tp": world, "ms_per_token": round(ms, 4),
+            "layers": args.layers, "tp": world, "tp_impl": args.tp_impl if world > 1 or p2p else None,
+            "ms_per_token": round(ms, 4),
             "GBps_per_gpu": round(bytes_token / (ms * 1e-3) / 1e9, 1),
             "weight_bytes_per_gpu": int(bytes_token), "allreduces_per_token": 2 * args.layers if world > 1 else 0,
             "per_linear_us_eager": per, "finite": finite, "build_s": round(build_s, 1),
             "hbm_alloc_gb": round(mem_gb, 1), "parity_rel_l2_sampled": parity,
             "paper_context_ms": "A100 FT e2e per token, 3-bit row-wise: 51.6 (1 GPU), 35.8 (2), 27.2 (4), 24.2 (8) (Table 4 P:L475-478)",
         }), flush=True)
+    if p2p is not None:
+        p2p.close()
     if comm is not None:
         comm.close()
+    if world > 1:
         torch.distributed.destroy_process_group()
 
 

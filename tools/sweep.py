@@ -60,7 +60,16 @@ def time_product(ws_list, X, b, m, n, steps):
         graph.replay()
     e.record()
     torch.cuda.synchronize()
-    return a.elapsed_time(e) / (reps * G) * 1e3  # us per product
+    chain = a.elapsed_time(e) / (reps * G) * 1e3  # us per product in the graph chain
+    # isolated: events around each eager launch (no overlap with a neighbour)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(40)]
+    for i, (e0, e1) in enumerate(ev):
+        e0.record()
+        step(i)
+        e1.record()
+    torch.cuda.synchronize()
+    iso = float(np.median([e0.elapsed_time(e1) for e0, e1 in ev])) * 1e3
+    return chain, iso
 
 
 def case(name, m, n, q, g, b=1, uniform=False, steps=400, seed=7, compact=False):
@@ -79,14 +88,14 @@ def case(name, m, n, q, g, b=1, uniform=False, steps=400, seed=7, compact=False)
         alpha = torch.from_numpy(d["alpha"]).to(dev)
         ws_list = [L.lutgemm_pack_bcq(planes, alpha, None, n, g) for _ in range(ncopies)]
     X = torch.from_numpy(gen_x(seed, b, n)).to(dev)
-    us = time_product(ws_list, X, b, m, n, steps)
+    us, iso = time_product(ws_list, X, b, m, n, steps)
     peak = measured_peaks()["hbm_gbs"]
     gbs = B / (us * 1e-6) / 1e9
     lookups = m * q * (n // 8) * b
     lds_us = lookups / 32 / torch.cuda.get_device_properties(dev).multi_processor_count / SM_HZ * 1e6
     hbm_us = B / (peak * 1e9) * 1e6
     out = {"case": name, "m": m, "n": n, "q": q, "g": g, "b": b, "offset": offset, "compact": compact,
-           "us": round(us, 3),
+           "us": round(us, 3), "iso_us": round(iso, 3), "frac_hbm_iso": round(B / (iso * 1e-6) / 1e9 / measured_peaks()["hbm_gbs"], 4),
            "GBps": round(gbs, 1), "frac_hbm": round(gbs / peak, 4), "bytes_alg": B,
            "hbm_roof_us": round(hbm_us, 2), "lds_roof_us": round(lds_us, 2),
            "bound": "hbm" if hbm_us >= lds_us else "lds",
