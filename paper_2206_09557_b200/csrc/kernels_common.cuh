@@ -19,7 +19,11 @@ namespace lg {
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMiscBytes = 8192;       // x double buffer (2 x 2 KB) + mbarriers + flags
-constexpr int kSmemBytes = 227 * 1024;  // LUT (128 KB) on a 64 KB boundary + misc + weight prefetch area
+// LUT (128 KB) on a 64 KB boundary + misc + weight prefetch area = the opt-in maximum per CTA (227 KB),
+// which includes static shared memory: the product kernels declare none (tests/test_abi_cpu.py checks
+// the SASS resource usage)
+constexpr int kSmemBytes = 227 * 1024;
+constexpr int kMiscArrive = 4128;      // misc-block offset of the fused reduction's arrival slot (u32)
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kFusedMaxJ = 256;        // max CTAs per slice in the fused-reduction mode
 

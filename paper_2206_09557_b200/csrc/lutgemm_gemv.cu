@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     // at once (their SMs go to the next kernel), the last R wait for the group
     // and each sums 1/R of its rows over the S slices in slice order
     // (deterministic, R11).  R = p.reducers (1 <= R <= S).
-    __shared__ unsigned s_k;
+    unsigned& s_k = *reinterpret_cast<unsigned*>(sm.misc_p + kMiscArrive);  // no static shared memory
     const int fj = blockIdx.x % J;
     const int R = max(1, min(p.reducers, sh.S));
     unsigned* arrive = p.counters + fj;

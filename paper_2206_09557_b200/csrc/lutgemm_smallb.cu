@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemvv_kernel(const KParams p)
     ++e;
   }
   if (J > 0) {  // fused arrival-ordered reduction over the SV sub-slices (as in lut_gemv_kernel)
-    __shared__ unsigned s_k;
+    unsigned& s_k = *reinterpret_cast<unsigned*>(sm.misc_p + kMiscArrive);  // no static shared memory
     const int fj = blockIdx.x % J;
     const int R = max(1, min(p.reducers, SV));
     unsigned* arrive = p.counters + fj;

@@ -36,6 +36,21 @@ def test_library_is_sm100a_only():
     assert all("sm_100a" in line for line in out.splitlines() if "ELF" in line)
 
 
+def test_product_kernels_fit_the_shared_memory_opt_in():
+    """The product kernels request 227 KB of dynamic shared memory, the per-CTA opt-in maximum; any
+    static __shared__ variable on top (beyond the 1 KB the system reserves per CTA) makes every launch
+    fail with cudaErrorInvalidValue, so none may declare one."""
+    import subprocess
+    import paper_2206_09557_b200.lutgemm as B
+    out = subprocess.run(["cuobjdump", "-res-usage", B.LIB_PATH], capture_output=True, text=True).stdout
+    found = 0
+    for name, shared in re.findall(r"Function (\S+):\s*\n\s*REG:\d+ STACK:\d+ SHARED:(\d+)", out):
+        if re.search(r"lut_gemv_kernel|lut_gemvv_kernel|lut_gemm_batched_kernel", name):
+            found += 1
+            assert int(shared) <= 1024, (name, shared)
+    assert found >= 45
+
+
 def test_abi_version_and_sizes():
     import paper_2206_09557_b200 as L
     from paper_2206_09557_b200.lutgemm import lib
