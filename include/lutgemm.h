@@ -26,12 +26,15 @@
  *  - The library is stateless except for an explicit TP communicator and the
  *    thread-local error text; calls on distinct outputs/workspaces are
  *    thread-safe.
- *  - Supported shapes on the GPU path: n % 32 == 0, n % g == 0 and
- *    g in {32, 64, 128, 256, 512, 1024} or g a multiple of 1024 or g == n (any n)
- *    (g == n is row-wise, P:L496 '-' / P:L392 "g=m"); 1 <= q <= 8, m >= 1,
- *    1 <= b <= 32.  Anything else returns LUTGEMM_ERR_INVALID_ARG (DESIGN.md
- *    reading R13: the paper does not define chunks straddling a group; the
- *    power-of-two rule keeps every group inside one 1024-column LUT slice).
+ *  - Supported shapes: n % 8 == 0, g % 8 == 0, n % g == 0
+ *    (g is "an arbitrary number of weights"; g == n is row-wise,
+ *    P:L496 '-' / P:L392 "g=m"); 1 <= q <= 8, m >= 1, 1 <= b <= 32.  Anything
+ *    else returns LUTGEMM_ERR_INVALID_ARG.  A mu = 8 chunk never straddles a
+ *    group under this rule (R13).  Groups that are not a multiple of
+ *    32 columns (g % 32 != 0, e.g. 8, 24, 40) split a 32-column word: those
+ *    weights store one scale entry per 8-column chunk and run the generic-q
+ *    kernels (correct, untuned); the UNIFORM_COMPACT format and the
+ *    quantizers need g % 32 == 0 (and the quantizers n % 32 == 0).
  *  - Requires an sm_100 device (B200); otherwise LUTGEMM_ERR_UNSUPPORTED.
  */
 #ifndef LUTGEMM_H_
@@ -146,7 +149,7 @@ lutgemm_status lutgemm_unpack_bcq(const lutgemm_weight* w, uint32_t* planes, uin
 
 /* ---- Quantizers (the offline step before the path) ----
  * Input: a dense weight W, device fp16 [m][n] row-major; same shape rules as
- * every call (n % 32 == 0, g as above).  Outputs are the canonical pack
+ * every call plus n % 32 == 0 and g % 32 == 0.  Outputs are the canonical pack
  * sources above (device buffers, caller-owned), so a dense layer becomes a
  * packed weight with quantize_* followed by lutgemm_pack_bcq.  Offline,
  * asynchronous on `stream`, deterministic.

@@ -19,10 +19,12 @@ namespace lg {
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMiscBytes = 8192;       // x double buffer (2 x 2 KB) + mbarriers + flags
-// LUT (128 KB) on a 64 KB boundary + misc + weight prefetch area = the opt-in maximum per CTA (227 KB),
-// which includes static shared memory: the product kernels declare none (tests/test_abi_cpu.py checks
-// the SASS resource usage)
-constexpr int kSmemBytes = 227 * 1024;
+// dynamic shared memory per CTA: the LUT (128 KB) on a 64 KB boundary + misc for any base alignment.
+// The opt-in maximum (227 KB) includes static shared memory; the product kernels declare none
+// (tests/test_abi_cpu.py checks the SASS resource usage).  A 227 KB variant with a weight prefetch
+// area before the PDL wait measured slower everywhere (measured and dropped).
+constexpr int kSmemBytes = 227 * 1024;     // the attribute set on every product kernel (upper bound)
+constexpr int kSmemBytesBase = 3 * 65536;  // what the launches request
 constexpr int kMiscArrive = 4128;      // misc-block offset of the fused reduction's arrival slot (u32)
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kFusedMaxJ = 256;        // max CTAs per slice in the fused-reduction mode
@@ -31,26 +33,13 @@ struct SmemMap {
   uint32_t lut;     // shared-window address of the LUT (multiple of 64 KB)
   uint32_t misc;    // shared-window address of the misc block
   uint8_t* misc_p;  // generic pointer to the misc block
-  uint32_t fa, fa_bytes, fb, fb_bytes;  // the two free areas (weight prefetch), 16-byte aligned
 };
 
-__device__ __forceinline__ SmemMap map_smem(uint8_t* smem) {
+__device__ __forceinline__ SmemMap map_smem(uint8_t* smem, int /*bytes*/) {
   SmemMap m;
-  const uint32_t base = smem_u32(smem), end = base + (uint32_t)kSmemBytes;
+  const uint32_t base = smem_u32(smem);
   m.lut = (base + 0xFFFFu) & ~0xFFFFu;
-  if (m.lut - base >= (uint32_t)kMiscBytes) {  // [base, misc) [.. free A ..) [LUT) [.. free B ..)
-    m.misc = base;
-    m.fa = base + kMiscBytes;
-    m.fb = m.lut + kLutBytes;
-  } else {                                      // [small gap) [LUT) [misc) [.. free B ..)
-    m.misc = m.lut + kLutBytes;
-    m.fa = base;
-    m.fb = m.misc + kMiscBytes;
-  }
-  m.fa = (m.fa + 15u) & ~15u;
-  m.fb = (m.fb + 15u) & ~15u;
-  m.fa_bytes = m.lut > m.fa ? m.lut - m.fa : 0u;
-  m.fb_bytes = end > m.fb ? end - m.fb : 0u;
+  m.misc = (m.lut - base >= (uint32_t)kMiscBytes) ? base : m.lut + kLutBytes;
   m.misc_p = smem + (m.misc - base);
   return m;
 }
@@ -119,11 +108,12 @@ __device__ __forceinline__ float reduce4(f32x2 a01, f32x2 a23, int lane) {
   return k;
 }
 
-// Stage x[beta][col0 .. col0 + 32*nl) for beta < nb into buf[beta][0 .. 32*P)
-// (fp16), zero-filling lanes >= nl and batch rows nb..B-1.  Called by warp 0.
-__device__ __forceinline__ void stage_x(__half* buf, uint32_t bar, const __half* x, int n, int col0, int nl,
+// Stage x[beta][col0 .. col0 + nc) for beta < nb into buf[beta][0 .. 32*P)
+// (fp16), zero-filling columns >= nc (nc % 8 == 0: whole 16-byte units) and
+// batch rows nb..B-1.  Called by warp 0.
+__device__ __forceinline__ void stage_x(__half* buf, uint32_t bar, const __half* x, int n, int col0, int nc,
                                         int P, int nb, int B, int lane) {
-  const uint32_t bytes = (uint32_t)nl * 64u;
+  const uint32_t bytes = (uint32_t)nc * 2u;
   if (lane == 0) {
     fence_proxy_async_smem();
     mbar_arrive_expect_tx(bar, bytes * (uint32_t)nb);
@@ -133,7 +123,7 @@ __device__ __forceinline__ void stage_x(__half* buf, uint32_t bar, const __half*
   // zero-fill the rest (generic proxy, disjoint from the async writes)
   const int row_h = 32 * P;
   for (int beta = 0; beta < B; ++beta) {
-    const int from = beta < nb ? 32 * nl : 0;
+    const int from = beta < nb ? nc : 0;
     for (int e = from + lane * 8; e < row_h; e += 32 * 8)
       *reinterpret_cast<uint4*>(buf + (size_t)beta * row_h + e) = make_uint4(0, 0, 0, 0);
   }
@@ -146,6 +136,8 @@ struct Ring {
   uint4 k[QT];
   uint2 a[QT];
   uint2 z;
+  const uint8_t* ap;  // chunk-group shapes (kGrpChunk, QT = 8 only): the quad's scale / z addresses,
+  const uint8_t* zp;  // read at compute time (ring_compute_cg)
 };
 
 // Per-segment addressing of a lane's fields in the three slice regions.
@@ -159,7 +151,7 @@ struct LaneAddr {
 
 __device__ __forceinline__ LaneAddr lane_addr(const Shape& sh, const uint8_t* data, int s, int Ls, int lay) {
   LaneAddr a;
-  const int k = lane_group(sh, lay);
+  const int k = lane_group(sh, s, lay);
   a.kp = data + key_at(sh, s, Ls, 0, 0, lay, 0);
   a.ap = data + alpha_at(sh, s, Ls, 0, 0, k, 0);
   a.zp = data + z_at(sh, s, Ls, 0, k, 0);
@@ -205,6 +197,40 @@ __device__ __forceinline__ void ring_compute(const Ring<QT>& r, uint32_t lc, flo
     const f32x2 xs = pack2(xsum, xsum);
     acc01 = fma2(h2_to_f32x2(r.z.x), xs, acc01);
     acc23 = fma2(h2_to_f32x2(r.z.y), xs, acc23);
+  }
+}
+
+// Chunk-group shapes (g % 32 != 0, kGrpChunk; generic-q kernels only): every 8-column chunk of the
+// lane's word has its own scale entry, so each lookup is scaled on its own:
+//   acc[r] = sum_i sum_j alpha[r][chunk j][i] * T_{4l+j}[key_ij(r)]  (+ sum_j z[r][chunk j] * xsum_j)
+// The scales (32 contiguous bytes per plane: chunks 0..3 x rows 0..3) and z are loaded here, not
+// through the register ring: a correct, untuned path for the rare group sizes.
+template <bool HAS_Z>
+__device__ __forceinline__ void ring_compute_cg(const Ring<8>& r, uint32_t lc, const float (&xs)[4], f32x2& acc01,
+                                                f32x2& acc23, int q) {
+  acc01 = 0ull;
+  acc23 = 0ull;
+  for (int i = 0; i < q; ++i) {
+    const uint4 A0 = ldg_nc_u4(r.ap + 32 * i), A1 = ldg_nc_u4(r.ap + 32 * i + 16);
+    const uint4 w = r.k[i];
+    acc01 = fma2(h2_to_f32x2(A0.x), pack2(lut1<0>(w.x, lc), lut1<0>(w.y, lc)), acc01);
+    acc23 = fma2(h2_to_f32x2(A0.y), pack2(lut1<0>(w.z, lc), lut1<0>(w.w, lc)), acc23);
+    acc01 = fma2(h2_to_f32x2(A0.z), pack2(lut1<1>(w.x, lc), lut1<1>(w.y, lc)), acc01);
+    acc23 = fma2(h2_to_f32x2(A0.w), pack2(lut1<1>(w.z, lc), lut1<1>(w.w, lc)), acc23);
+    acc01 = fma2(h2_to_f32x2(A1.x), pack2(lut1<2>(w.x, lc), lut1<2>(w.y, lc)), acc01);
+    acc23 = fma2(h2_to_f32x2(A1.y), pack2(lut1<2>(w.z, lc), lut1<2>(w.w, lc)), acc23);
+    acc01 = fma2(h2_to_f32x2(A1.z), pack2(lut1<3>(w.x, lc), lut1<3>(w.y, lc)), acc01);
+    acc23 = fma2(h2_to_f32x2(A1.w), pack2(lut1<3>(w.z, lc), lut1<3>(w.w, lc)), acc23);
+  }
+  if (HAS_Z) {
+    const uint4 Z0 = ldg_nc_u4(r.zp), Z1 = ldg_nc_u4(r.zp + 16);
+    const uint32_t zc[8] = {Z0.x, Z0.y, Z0.z, Z0.w, Z1.x, Z1.y, Z1.z, Z1.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const f32x2 xx = pack2(xs[j], xs[j]);
+      acc01 = fma2(h2_to_f32x2(zc[2 * j]), xx, acc01);
+      acc23 = fma2(h2_to_f32x2(zc[2 * j + 1]), xx, acc23);
+    }
   }
 }
 
@@ -343,21 +369,25 @@ struct VPtr {
 };
 
 template <int QT, int ZM>
-__device__ __forceinline__ void vring_load(Ring<QT>& r, bool ok, VPtr& pt, int q) {
+__device__ __forceinline__ void vring_load(Ring<QT>& r, bool ok, VPtr& pt, int q, bool cg = false) {
   constexpr bool HAS_Z = ZM != 0, CMP = ZM == 2;  // z term; compact scales (alpha_i = 2^(i-1) s)
+  if (QT == 8) {  // chunk-group shapes read the scales at compute time (vring_compute_cg); null = skip
+    r.ap = ok ? pt.aq : nullptr;
+    r.zp = pt.zq;
+  }
 #pragma unroll
   for (int i = 0; i < QT; ++i) {
     if (QT <= 4 || i < q) {
       if (ok) {
         r.k[i] = ldg_stream_u4(pt.kq + i * pt.kstride);
-        r.a[i] = (!CMP || i == 0) ? ldg_nc_u2(pt.aq + 8 * i) : make_uint2(0, 0);
+        if (!cg) r.a[i] = (!CMP || i == 0) ? ldg_nc_u2(pt.aq + 8 * i) : make_uint2(0, 0);
       } else {
         r.k[i] = make_uint4(0, 0, 0, 0);
         r.a[i] = make_uint2(0, 0);
       }
     }
   }
-  if (HAS_Z) r.z = ok ? ldg_nc_u2(pt.zq) : make_uint2(0, 0);
+  if (HAS_Z && !cg) r.z = ok ? ldg_nc_u2(pt.zq) : make_uint2(0, 0);
   pt.kq += pt.KB;
   pt.aq += pt.AB;
   if (HAS_Z) pt.zq += pt.ZB;
@@ -416,6 +446,49 @@ __device__ __forceinline__ void vring_compute(const Ring<QT>& r, uint32_t lc, co
 #pragma unroll
       for (int p = 0; p < NP; ++p) acc[rho][p] = fma2(zz, xs[p], acc[rho][p]);
     }
+  }
+}
+
+// chunk-group shapes (kGrpChunk, generic-q kernels): acc[rho][p] += sum_i sum_J alpha[rho][J][i] *
+// (lookups of chunk J) + sum_J z[rho][J] * xs[J] -- each chunk of the lane's word scaled on its own
+// (see ring_compute_cg); the scales are read here (32 contiguous bytes per plane)
+template <int V, bool HAS_Z>
+__device__ __forceinline__ void vring_compute_cg(const Ring<8>& r, uint32_t lc, const f32x2 (&xs)[4][V / 2],
+                                                 f32x2 (&acc)[4][V / 2], int q) {
+  constexpr int NP = V / 2;
+  if (r.ap == nullptr) return;  // quad past the end
+  for (int i = 0; i < q; ++i) {
+    const uint4 A0 = ldg_nc_u4(r.ap + 32 * i), A1 = ldg_nc_u4(r.ap + 32 * i + 16);
+    const uint32_t aw[8] = {A0.x, A0.y, A0.z, A0.w, A1.x, A1.y, A1.z, A1.w};  // chunk J: rows 01 = 2J, 23 = 2J+1
+    const uint32_t kw[4] = {r.k[i].x, r.k[i].y, r.k[i].z, r.k[i].w};
+#pragma unroll
+    for (int rho = 0; rho < 4; ++rho) {
+      f32x2 t[4][NP];
+      vlut<V, 0>(kw[rho], lc, t[0]);
+      vlut<V, 1>(kw[rho], lc, t[1]);
+      vlut<V, 2>(kw[rho], lc, t[2]);
+      vlut<V, 3>(kw[rho], lc, t[3]);
+#pragma unroll
+      for (int J = 0; J < 4; ++J) {
+        const float2 a = h2_to_f2(aw[2 * J + (rho >> 1)]);
+        const float av = (rho & 1) ? a.y : a.x;
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp) acc[rho][pp] = fma2(pack2(av, av), t[J][pp], acc[rho][pp]);
+      }
+    }
+  }
+  if (HAS_Z) {
+    const uint4 Z0 = ldg_nc_u4(r.zp), Z1 = ldg_nc_u4(r.zp + 16);
+    const uint32_t zw[8] = {Z0.x, Z0.y, Z0.z, Z0.w, Z1.x, Z1.y, Z1.z, Z1.w};
+#pragma unroll
+    for (int rho = 0; rho < 4; ++rho)
+#pragma unroll
+      for (int J = 0; J < 4; ++J) {
+        const float2 zz = h2_to_f2(zw[2 * J + (rho >> 1)]);
+        const float zv = (rho & 1) ? zz.y : zz.x;
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp) acc[rho][pp] = fma2(pack2(zv, zv), xs[J][pp], acc[rho][pp]);
+      }
   }
 }
 
@@ -509,7 +582,7 @@ int num_sms();
 cudaError_t ensure_smem_attr(const void* kernel);  // dynamic-smem opt-in, once per (kernel, device)
 const cudaLaunchAttribute* pdl_attr();              // programmatic stream serialization
 
-// one product kernel launch: PDL attribute, kSmemBytes of dynamic shared memory
+// one product kernel launch: PDL attribute, p.smem_bytes of dynamic shared memory
 template <typename K>
 inline cudaError_t launch(K kernel, int grid, const KParams& p, cudaStream_t st, int threads = kThreads) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -518,7 +591,7 @@ inline cudaError_t launch(K kernel, int grid, const KParams& p, cudaStream_t st,
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(threads);
-  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.dynamicSmemBytes = p.smem_bytes > 0 ? p.smem_bytes : kSmemBytesBase;
   cfg.stream = st;
   cfg.attrs = const_cast<cudaLaunchAttribute*>(pdl_attr());
   cfg.numAttrs = 1;
@@ -546,6 +619,10 @@ inline cudaError_t dispatch_qz(const KParams& p, int grid, cudaStream_t st) {
       default: return F<8, ZM>::run(p, grid, st);
     }
   };
+  if (p.sh.gcls == kGrpChunk) {  // per-chunk scales: the generic-q kernels only (ring_compute_cg)
+    if (p.sh.has_z) return F<8, 1>::run(p, grid, st);
+    return F<8, 0>::run(p, grid, st);
+  }
   if (p.sh.compact) return byq(std::integral_constant<int, 2>{});
   if (p.sh.has_z) return byq(std::integral_constant<int, 1>{});
   return byq(std::integral_constant<int, 0>{});

@@ -30,14 +30,21 @@ bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) %
 
 lutgemm_status check_shape(int m, int n, int q, int g) {
   if (m < 1) return fail(LUTGEMM_ERR_INVALID_ARG, "m=%d must be >= 1", m);
-  if (n < 32 || n % 32) return fail(LUTGEMM_ERR_INVALID_ARG, "n=%d must be a positive multiple of 32", n);
+  // n % 8, g % 8, g | n (g == n: row-wise); mu = 8 chunks never straddle a group (R13)
+  if (n < 8 || n % 8) return fail(LUTGEMM_ERR_INVALID_ARG, "n=%d must be a positive multiple of 8", n);
   if (q < 1 || q > 8) return fail(LUTGEMM_ERR_INVALID_ARG, "q=%d must be in [1, 8]", q);
-  // a power of two up to one LUT slice, whole slices, or row-wise (g == n, any multiple of 32)
-  const bool g_ok = (g >= 32 && g <= 1024 && (1024 % g) == 0) || (g > 1024 && g % 1024 == 0) || g == n;
-  if (!g_ok || n % g)
+  if (g < 8 || g % 8 || n % g)
+    return fail(LUTGEMM_ERR_INVALID_ARG, "g=%d must be a positive multiple of 8 that divides n=%d", g, n);
+  if ((long long)m * ((n + 31) / 32) >= (1LL << 40)) return fail(LUTGEMM_ERR_INVALID_ARG, "shape too large");
+  return LUTGEMM_OK;
+}
+
+// the compact uniform format holds one scale per (row, 32-column lane) at most: its kernels scale a
+// lane's whole word by one s, so a group must not split a lane (g % 32 == 0 or row-wise)
+lutgemm_status check_compact(int n, int g) {
+  if (lg::group_class(n, g) == lg::kGrpChunk)
     return fail(LUTGEMM_ERR_INVALID_ARG,
-                "g=%d must divide n=%d and be one of 32..1024 (power of two), a multiple of 1024, or n", g, n);
-  if ((long long)m * (n / 32) >= (1LL << 40)) return fail(LUTGEMM_ERR_INVALID_ARG, "shape too large");
+                "the uniform-compact format needs g %% 32 == 0 or g == n (g=%d); pack with LUTGEMM_SRC_UNIFORM", g);
   return LUTGEMM_OK;
 }
 
@@ -73,6 +80,7 @@ lutgemm_status check_weight(const lutgemm_weight* w) {
     return fail(LUTGEMM_ERR_INVALID_ARG, "bad weight format %d", w->format);
   if (w->format == LUTGEMM_FMT_UNIFORM_COMPACT && !w->has_offset)
     return fail(LUTGEMM_ERR_INVALID_ARG, "the uniform-compact format carries an offset (has_offset = 1)");
+  if (w->format == LUTGEMM_FMT_UNIFORM_COMPACT) return check_compact(w->n, w->g);
   return LUTGEMM_OK;
 }
 
@@ -130,6 +138,7 @@ lutgemm_status lutgemm_packed_bytes_fmt(int m, int n, int q, int g, int has_offs
   if (!bytes) return fail(LUTGEMM_ERR_INVALID_ARG, "bytes is NULL");
   if (format != LUTGEMM_FMT_BCQ && format != LUTGEMM_FMT_UNIFORM_COMPACT)
     return fail(LUTGEMM_ERR_INVALID_ARG, "bad format %d", format);
+  if (format == LUTGEMM_FMT_UNIFORM_COMPACT && (st = check_compact(n, g)) != LUTGEMM_OK) return st;
   *bytes = lg::packed_bytes(lg::make_shape(m, n, q, g, has_offset, format == LUTGEMM_FMT_UNIFORM_COMPACT));
   return LUTGEMM_OK;
 }
@@ -141,6 +150,7 @@ lutgemm_status lutgemm_pack_bcq(const lutgemm_pack_src* src, lutgemm_weight* dst
   const bool compact = src->kind == LUTGEMM_SRC_UNIFORM_COMPACT;
   const bool uniform = src->kind == LUTGEMM_SRC_UNIFORM || compact;
   if (src->kind != LUTGEMM_SRC_BCQ && !uniform) return fail(LUTGEMM_ERR_INVALID_ARG, "bad src kind %d", src->kind);
+  if (compact && (st = check_compact(src->n, src->g)) != LUTGEMM_OK) return st;
   if (uniform) {
     if (!src->codes || !src->scale || !src->zero)
       return fail(LUTGEMM_ERR_INVALID_ARG, "uniform source needs codes, scale and zero");
@@ -186,7 +196,7 @@ lutgemm_status lutgemm_unpack_bcq(const lutgemm_weight* w, uint32_t* planes, uin
 }
 
 size_t lutgemm_workspace_bytes(int m, int n, int b) {
-  if (m < 1 || n < 32 || b < 1) return 0;
+  if (m < 1 || n < 8 || b < 1) return 0;
   const lg::Shape sh = lg::make_shape(m, n, 1, n, 0);
   return lg::workspace_bytes(sh, b);
 }
@@ -253,6 +263,8 @@ lutgemm_status lutgemm_quantize_rtn(const uint16_t* W, int m, int n, int q, int 
                                     uint16_t* zero, void* stream) {
   lutgemm_status st = check_shape(m, n, q, g);
   if (st != LUTGEMM_OK) return st;
+  if (n % 32 || g % 32)  // the quantizers work on whole 32-column words (one warp lane per column)
+    return fail(LUTGEMM_ERR_INVALID_ARG, "the quantizers need n %% 32 == 0 and g %% 32 == 0 (n=%d, g=%d)", n, g);
   if (!W || !codes || !scale || !zero) return fail(LUTGEMM_ERR_INVALID_ARG, "W, codes, scale and zero must be non-NULL");
   if (!aligned(W, 2) || !aligned(scale, 2) || !aligned(zero, 2))
     return fail(LUTGEMM_ERR_MISALIGNED, "fp16 buffers must be 2-byte aligned");
@@ -267,6 +279,8 @@ lutgemm_status lutgemm_quantize_bcq(const uint16_t* W, int m, int n, int q, int 
                                     uint16_t* alpha, void* stream) {
   lutgemm_status st = check_shape(m, n, q, g);
   if (st != LUTGEMM_OK) return st;
+  if (n % 32 || g % 32)
+    return fail(LUTGEMM_ERR_INVALID_ARG, "the quantizers need n %% 32 == 0 and g %% 32 == 0 (n=%d, g=%d)", n, g);
   if (iters < 0 || iters > 1000) return fail(LUTGEMM_ERR_INVALID_ARG, "iters=%d must be in [0, 1000]", iters);
   if (!W || !planes || !alpha) return fail(LUTGEMM_ERR_INVALID_ARG, "W, planes and alpha must be non-NULL");
   if (!aligned(W, 2) || !aligned(planes, 4) || !aligned(alpha, 2))

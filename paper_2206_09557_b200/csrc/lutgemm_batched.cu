@@ -18,6 +18,7 @@ __global__ void __launch_bounds__(NTH, 1) lut_gemm_batched_kernel(const KParams 
   const int warp = __shfl_sync(kFull, tid >> 5, 0);
   const Shape sh = p.sh;
   const int q = QT <= 4 ? QT : sh.q;
+  const bool cg = QT == 8 && sh.gcls == kGrpChunk;  // per-chunk scales (vring_compute_cg)
   const int NV = p.nv, NW = LR / NV, bpad = V * NV, b = p.b, spi = p.spi;
   const int qi = lane / LR, wv = lane % LR, w = wv / NV, v = wv % NV;
   const int rbq = (NTH / 32) * QPW;  // row quads per work item
@@ -26,12 +27,11 @@ __global__ void __launch_bounds__(NTH, 1) lut_gemm_batched_kernel(const KParams 
   const int it1 = (int)(p.items * (blockIdx.x + 1) / gridDim.x);
   if (it0 >= it1) return;
 
-  const SmemMap sm = map_smem(smem);
+  const SmemMap sm = map_smem(smem, p.smem_bytes > 0 ? p.smem_bytes : kSmemBytesBase);
   const __half* xtile0 = reinterpret_cast<const __half*>(sm.misc_p);
   const __half* xtile1 = reinterpret_cast<const __half*>(sm.misc_p + 2048);
   const uint32_t xt0 = sm.misc, xt1 = sm.misc + 2048;
   const uint32_t lc = (sm.lut & 0xFFFF0000u) | ((uint32_t)((LR + wv) * 4 * V) << 8) | (uint32_t)(wv * 4 * V);
-  const int gsh = p.gsh;  // layout lane p's group in the slice = p >> gsh
 
   auto nsub_of = [&](int s) { return (slice_lanes(sh.n, s) + NW - 1) / NW; };
   auto first_step = [&](int it) {
@@ -57,10 +57,9 @@ __global__ void __launch_bounds__(NTH, 1) lut_gemm_batched_kernel(const KParams 
   // for the first 128 threads (2 KB), x is L2-resident
   auto load_x = [&](uint32_t dst, const VStep& st) {
     if (tid < 128) {
-      const int Ls = slice_lanes(sh.n, st.s);
       const int per_row = 4 * NW;  // 16-byte cells per tile row
       const int bt = tid / per_row, c = tid % per_row;
-      const bool ok = bt < b && st.k * NW + c / 4 < Ls;
+      const bool ok = bt < b && 32 * st.k * NW + 8 * c < slice_cols(sh.n, st.s);  // zero past n
       const __half* src = ok ? p.x + (size_t)bt * sh.n + st.s * kSliceCols + 32 * st.k * NW + 8 * c : p.x;
       cp_async_16(dst + 16u * (uint32_t)xcell<V>(c, bt, NV), src, ok ? 16u : 0u);
     }
@@ -79,8 +78,9 @@ __global__ void __launch_bounds__(NTH, 1) lut_gemm_batched_kernel(const KParams 
     pt.ZB = ZB * V;
     pt.kstride = (uint32_t)Ls * 16u;
     pt.kq = p.data + keys_base(sh, st.s, Ls) + (size_t)rq * KB + pl * 16;
-    pt.aq = p.data + alpha_base(sh, st.s, Ls) + (size_t)rq * AB + (uint32_t)(pl >> gsh) * scale_planes(sh) * 8u;
-    pt.zq = p.data + z_base(sh, st.s, Ls) + (size_t)rq * ZB + (uint32_t)(pl >> gsh) * 8u;
+    const int k = lane_group(sh, st.s, pl);
+    pt.aq = p.data + alpha_at(sh, st.s, Ls, rq, 0, k, 0);
+    pt.zq = p.data + z_at(sh, st.s, Ls, rq, k, 0);
     return pt;
   };
   Ring<QT> ring[NB];
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(NTH, 1) lut_gemm_batched_kernel(const KParams 
     const int rq_w = (st.it % NRB) * rbq + warp * QPW;
     nxt = lane_ptr(st, rq_w, nxt_ok);
 #pragma unroll
-    for (int d = 0; d < PD; ++d) vring_load<QT, ZM>(ring[d], nxt_ok && rq_w + V * d + qi < sh.RQ, nxt, q);
+    for (int d = 0; d < PD; ++d) vring_load<QT, ZM>(ring[d], nxt_ok && rq_w + V * d + qi < sh.RQ, nxt, q, cg);
   };
 
   VStep st = first_step(it0);
@@ -122,10 +122,22 @@ __global__ void __launch_bounds__(NTH, 1) lut_gemm_batched_kernel(const KParams 
       if (sn.it < it1) load_x((e & 1) ? xt0 : xt1, sn);  // lands during the lookups
       f32x2 xs[NP];
       if (HAS_Z) vword<V>(0xFFFFFFFFu, lc, xs);  // sum of x over the lane's 32 columns = sum_J T_J[255]
+      f32x2 xsJ[4][NP];                          // chunk-group shapes: per chunk
+      if (QT == 8 && HAS_Z && cg) {
+        vlut<V, 0>(0xFFFFFFFFu, lc, xsJ[0]);
+        vlut<V, 1>(0xFFFFFFFFu, lc, xsJ[1]);
+        vlut<V, 2>(0xFFFFFFFFu, lc, xsJ[2]);
+        vlut<V, 3>(0xFFFFFFFFu, lc, xsJ[3]);
+      }
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
-        if (t + PD < NT) vring_load<QT, ZM>(ring[(t + PD) % NB], lane_ok && V * (t + PD) < nql, cur, q);
-        vring_compute<V, QT, ZM>(ring[t % NB], lc, xs, acc[t], q);
+        if (t + PD < NT) vring_load<QT, ZM>(ring[(t + PD) % NB], lane_ok && V * (t + PD) < nql, cur, q, cg);
+        if constexpr (QT == 8) {
+          if (cg) vring_compute_cg<V, HAS_Z>(ring[t % NB], lc, xsJ, acc[t], q);
+          else vring_compute<V, QT, ZM>(ring[t % NB], lc, xs, acc[t], q);
+        } else {
+          vring_compute<V, QT, ZM>(ring[t % NB], lc, xs, acc[t], q);
+        }
       }
       if (sn.it < it1) prologue(sn);  // next step's first quads fly during the barrier and rebuild
       cp_async_wait_all();

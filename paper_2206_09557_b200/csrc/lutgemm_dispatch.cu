@@ -110,7 +110,7 @@ cudaError_t run_gemv_p2p(const Shape& sh, const void* data, const uint16_t* x, v
 
 static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint16_t* x, int b, uint16_t* y, float* yf,
                                   void* ws, cudaStream_t st, const P2PArgs* pa) {
-  KParams p;
+  KParams p{};
   p.p2p_mode = pa ? pa->mode : 0;
   p.npeers = pa ? pa->npeers : 0;
   p.yoff = pa ? pa->yoff : 0;
@@ -139,11 +139,6 @@ static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint1
   p.spi = 1;
   p.qpw = 256;
   {
-    int gs = 0;  // layout lane -> group shift (lanes are 32 columns); g > 1024: one group per slice
-    while (gs < 5 && (32 << gs) < sh.g) ++gs;
-    p.gsh = sh.g <= kSliceCols ? gs : 31;
-  }
-  {
     static unsigned seq = 0;  // consecutive launches alternate between two halves of the trace buffer
     p.trace = g_trace_on ? g_trace + (size_t)(seq++ & 1u) * (kTraceMaxCtas / 2) * kTraceSlots : nullptr;
   }
@@ -151,7 +146,8 @@ static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint1
   p.s2 = 0;
   if (!batched) {
     p.items = (long long)sh.S * sh.RQ;
-  } else if (b <= 4 && !(getenv("LUTGEMM_SMALLB_BATCHED") && atoi(getenv("LUTGEMM_SMALLB_BATCHED")))) {
+  } else if (b <= 4 && sh.gcls != kGrpChunk &&
+             !(getenv("LUTGEMM_SMALLB_BATCHED") && atoi(getenv("LUTGEMM_SMALLB_BATCHED")))) {
     // b <= 4: GEMV-structured kernel over sub-slices of 1024 / V columns, V = 2 (b = 2)
     // or 4 (b = 3, 4); LUTGEMM_SMALLB_BATCHED=1 selects the vector-slot batched kernel
     const int V = b == 2 ? 2 : 4;
@@ -181,12 +177,7 @@ static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint1
     }
   }
   p.fused_pair = pa ? 1 : 0;  // P2P epilogue: 8-row units, so row-quad groups start at even quads
-  {
-    static const int pf = getenv("LUTGEMM_SMEM_PF") ? atoi(getenv("LUTGEMM_SMEM_PF")) : 1 << 20;
-    static const unsigned l2 = getenv("LUTGEMM_L2_PF") ? (unsigned)atoi(getenv("LUTGEMM_L2_PF")) : 0u;
-    p.smem_pf = pf;
-    p.l2_pf = l2;
-  }
+  p.smem_bytes = kSmemBytesBase;
   if (!batched) {
     const int sms = num_sms();
     const int J = sh.S <= sms ? sms / sh.S : 0;

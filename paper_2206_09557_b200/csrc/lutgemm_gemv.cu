@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
   const int warp = __shfl_sync(kFull, tid >> 5, 0);  // warp-uniform for the compiler
   const Shape sh = p.sh;
   const int q = QT <= 4 ? QT : sh.q;
+  const bool cg = QT == 8 && sh.gcls == kGrpChunk;  // per-chunk scales (ring_compute_cg)
   const int J = p.fused_J;
   long long it0, it1;
   if (J > 0) {
@@ -260,15 +261,14 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
   // grid's CTAs exit and stream their first weights before their own PDL wait
   if (J > 0) pdl_launch_dependents();
 
-  const SmemMap sm = map_smem(smem);
+  const SmemMap sm = map_smem(smem, p.smem_bytes > 0 ? p.smem_bytes : kSmemBytesBase);
   __half* xbuf0 = reinterpret_cast<__half*>(sm.misc_p);
   __half* xbuf1 = reinterpret_cast<__half*>(sm.misc_p + 2048);
-  const uint32_t bar0 = sm.misc + 4096, bar1 = sm.misc + 4104, bar_pf = sm.misc + 4112;
+  const uint32_t bar0 = sm.misc + 4096, bar1 = sm.misc + 4104;
   const uint32_t lc = (sm.lut & 0xFFFF0000u) | ((uint32_t)(4 * lane + 128) << 8) | (uint32_t)(4 * lane);
   if (tid == 0) {
     mbar_init(bar0, 1);
     mbar_init(bar1, 1);
-    mbar_init(bar_pf, 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -296,59 +296,23 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     const uint8_t* lal = la.ap + (size_t)(rq_a + warp) * la.AB;
     const uint8_t* lz = la.zp + (size_t)(rq_a + warp) * la.ZB;
     int tl = 0;
-    // Fused mode, first segment: besides the PD register-ring quads, the KEYS (89 % of the bytes at
-    // q = 3, g = 128) of the next NB quads of every warp (quads rq_a + 16 PD .. + 16 (PD + NB)) are
-    // copied into shared memory by the bulk-copy engine at CTA start, before the PDL wait (weights
-    // only), so more of the weight stream is in flight while this CTA waits for the previous
-    // kernel and builds its LUT.  They feed one peeled ring iteration (their scales still come
-    // through the register ring); the quads go to the two free shared-memory areas, TA "rows" of
-    // 16 quads in the first.
-    bool pf = false;
-    uint32_t pfa = 0, pfb = 0;  // lane's key word of the first prefetched quad in area A / area B
-    int TA = 0;
-    if (QT <= 4 && e == 0 && J > 0 && p.smem_pf > 0 && (rq_b - rq_a) >= kWarps * (PD + NB)) {
-      const uint32_t rowb = (uint32_t)kWarps * la.KB;  // bytes of 16 quads' keys
-      TA = min((int)(sm.fa_bytes / rowb), NB);
-      pf = TA + (int)(sm.fb_bytes / rowb) >= NB;
-      if (pf) {
-        const uint32_t lo = (uint32_t)(lane_ok ? lane : 0) * 16u;
-        pfa = sm.fa + lo;
-        pfb = sm.fb + lo;
-        if (tid == 0) {
-          const uint8_t* src = p.data + keys_base(sh, s, Ls) + (size_t)(rq_a + kWarps * PD) * la.KB;
-          mbar_arrive_expect_tx(bar_pf, (uint32_t)NB * rowb);
-          if (TA > 0) bulk_g2s(sm.fa, src, (uint32_t)TA * rowb, bar_pf);
-          if (TA < NB) bulk_g2s(sm.fb, src + (size_t)TA * rowb, (uint32_t)(NB - TA) * rowb, bar_pf);
-        }
-      }
-      // optional L2 prefetch of the CTA's following key bytes (tuning knob)
-      if (p.l2_pf > 0 && tid == 0) {
-        const size_t kend = keys_base(sh, s, Ls) + (size_t)rq_b * la.KB;
-        const size_t k1 = keys_base(sh, s, Ls) + (size_t)(rq_a + kWarps * (PD + (pf ? NB : 0))) * la.KB;
-        const uint32_t nb = (uint32_t)min((size_t)p.l2_pf, kend > k1 ? kend - k1 : 0) & ~15u;
-        if (nb) bulk_prefetch_l2(p.data + k1, nb);
-      }
-    }
     Ring<QT> buf[NB];
-    // load quad tl of the warp into b: keys from global memory, or (smem >= 0) from prefetched
-    // row `smem` of the shared-memory area; scales always from global memory
-    auto load_quad = [&](Ring<QT>& b, int smem = -1) {
+    // load quad tl of the warp into b (keys, scales, z)
+    auto load_quad = [&](Ring<QT>& b) {
       if (nt == 0) return;  // a warp without quads in the segment loads nothing
-      if (smem >= 0) {
-        const uint32_t ka = (smem < TA ? pfa + (uint32_t)smem * kWarps * la.KB
-                                       : pfb + (uint32_t)(smem - TA) * kWarps * la.KB) + (uint32_t)warp * la.KB;
-#pragma unroll
-        for (int i = 0; i < QT; ++i)
-          if (QT <= 4 || i < q) b.k[i] = lds_u4(ka + (uint32_t)i * la.kstride);
-      } else {
-#pragma unroll
-        for (int i = 0; i < QT; ++i)
-          if (QT <= 4 || i < q) b.k[i] = ldg_stream_u4(lk + i * la.kstride);
-      }
 #pragma unroll
       for (int i = 0; i < QT; ++i)
-        if ((QT <= 4 || i < q) && (!CMP || i == 0)) b.a[i] = ldg_nc_u2(lal + 8 * i);
-      if (HAS_Z) b.z = ldg_nc_u2(lz);
+        if (QT <= 4 || i < q) b.k[i] = ldg_stream_u4(lk + i * la.kstride);
+      if (QT == 8) {
+        b.ap = lal;
+        b.zp = lz;
+      }
+      if (!cg) {
+#pragma unroll
+        for (int i = 0; i < QT; ++i)
+          if ((QT <= 4 || i < q) && (!CMP || i == 0)) b.a[i] = ldg_nc_u2(lal + 8 * i);
+        if (HAS_Z) b.z = ldg_nc_u2(lz);
+      }
       if (++tl < nt) {
         lk += (size_t)kWarps * la.KB;
         lal += (size_t)kWarps * la.AB;
@@ -366,7 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
       }
       pdl_wait();
       if (trace) trace[5] = globaltimer_ns();
-      if (warp == 0) stage_x(xbuf0, bar0, p.x, sh.n, s * kSliceCols, Ls, 32, 1, 1, lane);
+      if (warp == 0) stage_x(xbuf0, bar0, p.x, sh.n, s * kSliceCols, slice_cols(sh.n, s), 32, 1, 1, lane);
     }
     if (e > 0 || J == 0) {
 #pragma unroll
@@ -387,30 +351,31 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     if (warp == 0 && itn < it1) {
       const int sn = (int)(itn / sh.RQ);
       stage_x((e & 1) ? xbuf0 : xbuf1, (e & 1) ? bar0 : bar1, p.x, sh.n, sn * kSliceCols,
-              slice_lanes(sh.n, sn), 32, 1, 1, lane);
+              slice_cols(sh.n, sn), 32, 1, 1, lane);
     }
-    const float xsum = (HAS_Z && lane_ok) ? lane_xsum(sm.lut, lane) : 0.f;
+    const float xsum = (HAS_Z && lane_ok && !cg) ? lane_xsum(sm.lut, lane) : 0.f;
+    float xs4[4] = {0.f, 0.f, 0.f, 0.f};  // chunk-group shapes: x sum of each of the lane's chunks
+    if (QT == 8 && HAS_Z && cg && lane_ok) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) xs4[j] = lds_f32<0>(sm.lut + table_offset(lane, j) + 255u * 256u);
+    }
     // 4. main loop: per quad and plane 16 PRMT + 16 LDS + 6 FADD2 + 2 FFMA2, then
     //    a 6-shuffle transpose-reduce and one store per row of the slice partial
     float* pw = p.partial + (size_t)s * sh.m4 + 4 * (rq_a + warp) + (lane >> 3);  // this warp's next partial
     auto quad = [&](const Ring<QT>& b) {
       f32x2 acc01, acc23;
-      ring_compute<QT, ZM>(b, lc, xsum, acc01, acc23, q);
+      if constexpr (QT == 8) {
+        if (cg) ring_compute_cg<HAS_Z>(b, lc, xs4, acc01, acc23, q);
+        else ring_compute<QT, ZM>(b, lc, xsum, acc01, acc23, q);
+      } else {
+        ring_compute<QT, ZM>(b, lc, xsum, acc01, acc23, q);
+      }
       if (Ls < kLanesPerSlice && !lane_ok) acc01 = acc23 = 0ull;
       const float v = reduce4(acc01, acc23, lane);
       if ((lane & 7) == 0) *pw = v;
       pw += 4 * kWarps;
     };
     int t0 = 0;
-    if (pf) {  // peeled first iteration: quads PD .. PD + NB - 1 come from the shared-memory prefetch
-      mbar_wait(bar_pf, 0u);
-#pragma unroll
-      for (int d = 0; d < NB; ++d) {
-        load_quad(buf[(d + PD) % NB], d);
-        quad(buf[d]);
-      }
-      t0 = NB;
-    }
     for (; t0 + NB <= nt; t0 += NB) {
 #pragma unroll
       for (int d = 0; d < NB; ++d) {

@@ -23,11 +23,9 @@ struct KParams {
   int nv;            // batched: V-wide batch vectors per table entry slot group (b_pad = V * nv)
   int spi;           // batched: LUT slices per work item (split-K factor S2 = ceil(S / spi))
   int qpw;           // batched: row quads per work item (256 or 128)
-  int gsh;           // batched: layout lane -> slice-local group shift (31: one group per slice)
   int fused_J;       // GEMV: CTAs per slice in the fused-reduction mode (0: separate reduction kernel)
   int fused_pair;    // GEMV fused mode: row-quad group boundaries on even quads (8-row units)
-  int smem_pf;       // GEMV fused mode: max row quads per CTA prefetched into shared memory before the PDL wait
-  unsigned l2_pf;    // GEMV fused mode: weight bytes per CTA prefetched into L2 before the PDL wait
+  int smem_bytes;    // dynamic shared memory per CTA (0: kSmemBytesBase)
   int reducers;      // GEMV fused mode: the last R CTAs to arrive in a row-quad group reduce it
   // fused tensor-parallel epilogue over peer memory (NEXT-1, lutgemm_p2p.cu).  p2p_mode 1 (rows
   // all-gather): each finished fp16 row r goes to window[par][pr] + p2p_yarea + 2 (yoff + r) of every

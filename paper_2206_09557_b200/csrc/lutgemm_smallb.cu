@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemvv_kernel(const KParams p)
   if (it0 >= it1 && J == 0) return;
   if (J > 0) pdl_launch_dependents();
 
-  const SmemMap sm = map_smem(smem);
+  const SmemMap sm = map_smem(smem, p.smem_bytes > 0 ? p.smem_bytes : kSmemBytesBase);
   const uint32_t xt0 = sm.misc, xt1 = sm.misc + 2048;
   const __half* xtile0 = reinterpret_cast<const __half*>(sm.misc_p);
   const __half* xtile1 = reinterpret_cast<const __half*>(sm.misc_p + 2048);
@@ -41,10 +41,9 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemvv_kernel(const KParams p)
   auto load_x = [&](uint32_t dst, int hs) {
     if (tid < 128) {
       const int s = hs / V, h = hs % V;
-      const int Lh = min(LR, slice_lanes(sh.n, s) - LR * h);
       const int per_row = 4 * LR;
       const int bt = tid / per_row, c = tid % per_row;
-      const bool ok = bt < b && c / 4 < Lh;
+      const bool ok = bt < b && 32 * LR * h + 8 * c < slice_cols(sh.n, s);  // zero past n
       const __half* src = ok ? p.x + (size_t)bt * sh.n + s * kSliceCols + 32 * LR * h + 8 * c : p.x;
       cp_async_16(dst + 16u * (uint32_t)xcell<V>(c, bt, 1), src, ok ? 16u : 0u);
     }

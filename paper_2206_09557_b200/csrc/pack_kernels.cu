@@ -26,7 +26,7 @@ inline int blocks_for(size_t total) {
 }
 
 __global__ void pack_keys_kernel(const uint32_t* __restrict__ src, uint8_t* __restrict__ dst, Shape sh) {
-  const int nw = sh.n / 32;
+  const int nw = (sh.n + 31) / 32;
   const size_t total = (size_t)sh.q * sh.m4 * nw;
   for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
     const int w = (int)(idx % nw);
@@ -40,7 +40,7 @@ __global__ void pack_keys_kernel(const uint32_t* __restrict__ src, uint8_t* __re
 }
 
 __global__ void unpack_keys_kernel(const uint8_t* __restrict__ src, uint32_t* __restrict__ dst, Shape sh) {
-  const int nw = sh.n / 32;
+  const int nw = (sh.n + 31) / 32;
   const size_t total = (size_t)sh.q * sh.m * nw;
   for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
     const int w = (int)(idx % nw);
@@ -65,6 +65,7 @@ __global__ void pack_scales_kernel(const uint16_t* __restrict__ alpha, const uin
     const int Ls = slice_lanes(sh.n, s);
     if (k >= slice_groups(sh, Ls)) continue;
     const int grp = global_group(sh, s, k);
+    if (grp >= sh.G) continue;  // unused entry (kGrpSpan bound, kGrpChunk chunks past n): stays zero
     for (int r4 = 0; r4 < 4; ++r4) {
       const int r = 4 * rq + r4;
       for (int i = 0; i < sh.q; ++i)
@@ -74,17 +75,6 @@ __global__ void pack_scales_kernel(const uint16_t* __restrict__ alpha, const uin
         *reinterpret_cast<uint16_t*>(dst + z_at(sh, s, Ls, rq, k, r4)) =
             (r < sh.m && offset) ? offset[(size_t)r * sh.G + grp] : (uint16_t)0;
     }
-  }
-}
-
-// first slice that stores group grp, and the group's slice-local index
-__device__ inline void home_of_group(const Shape& sh, int grp, int* s, int* k) {
-  if (sh.g <= kSliceCols) {
-    *s = grp / (kSliceCols / sh.g);
-    *k = grp % (kSliceCols / sh.g);
-  } else {
-    *s = (int)(((long long)grp * sh.g) / kSliceCols);
-    *k = 0;
   }
 }
 
@@ -112,7 +102,7 @@ __global__ void unpack_scales_kernel(const uint8_t* __restrict__ src, uint16_t* 
 
 // uniform codes [m][n] -> keys: plane i word = bit i of 32 codes (b_hat_i, App. C)
 __global__ void pack_uniform_keys_kernel(const uint8_t* __restrict__ codes, uint8_t* __restrict__ dst, Shape sh) {
-  const int nw = sh.n / 32;
+  const int nw = (sh.n + 31) / 32;
   const size_t total = (size_t)sh.m4 * nw;
   for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
     const int w = (int)(idx % nw);
@@ -120,7 +110,8 @@ __global__ void pack_uniform_keys_kernel(const uint8_t* __restrict__ codes, uint
     uint32_t words[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (r < sh.m) {
       const uint8_t* c = codes + (size_t)r * sh.n + 32 * w;
-      for (int j = 0; j < 32; ++j) {
+      const int nc = min(32, sh.n - 32 * w);  // the last word may be partial (n % 32 != 0): padding bits 0
+      for (int j = 0; j < nc; ++j) {
         const uint32_t code = c[j];
         for (int i = 0; i < sh.q; ++i) words[i] |= ((code >> i) & 1u) << j;
       }
@@ -143,6 +134,7 @@ __global__ void pack_uniform_scales_kernel(const uint16_t* __restrict__ scale, c
     const int Ls = slice_lanes(sh.n, s);
     if (k >= slice_groups(sh, Ls)) continue;
     const int grp = global_group(sh, s, k);
+    if (grp >= sh.G) continue;  // unused entry: stays zero
     for (int r4 = 0; r4 < 4; ++r4) {
       const int r = 4 * rq + r4;
       double sv = 0.0, zh = 0.0;
@@ -172,7 +164,7 @@ cudaError_t run_pack_bcq(const Shape& sh, const uint32_t* planes, const uint16_t
                          void* dst, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(dst, 0, packed_bytes(sh), st);
   if (e != cudaSuccess) return e;
-  pack_keys_kernel<<<blocks_for((size_t)sh.q * sh.m4 * (sh.n / 32)), kPackThreads, 0, st>>>(
+  pack_keys_kernel<<<blocks_for((size_t)sh.q * sh.m4 * ((sh.n + 31) / 32)), kPackThreads, 0, st>>>(
       planes, static_cast<uint8_t*>(dst), sh);
   pack_scales_kernel<<<blocks_for((size_t)sh.S * sh.RQ * slice_groups(sh, kLanesPerSlice)), kPackThreads, 0, st>>>(
       alpha, offset, static_cast<uint8_t*>(dst), sh);
@@ -183,7 +175,7 @@ cudaError_t run_pack_uniform(const Shape& sh, const uint8_t* codes, const uint16
                              void* dst, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(dst, 0, packed_bytes(sh), st);
   if (e != cudaSuccess) return e;
-  pack_uniform_keys_kernel<<<blocks_for((size_t)sh.m4 * (sh.n / 32)), kPackThreads, 0, st>>>(
+  pack_uniform_keys_kernel<<<blocks_for((size_t)sh.m4 * ((sh.n + 31) / 32)), kPackThreads, 0, st>>>(
       codes, static_cast<uint8_t*>(dst), sh);
   pack_uniform_scales_kernel<<<blocks_for((size_t)sh.S * sh.RQ * slice_groups(sh, kLanesPerSlice)), kPackThreads, 0,
                                st>>>(scale, zero, static_cast<uint8_t*>(dst), sh);
@@ -193,7 +185,7 @@ cudaError_t run_pack_uniform(const Shape& sh, const uint8_t* codes, const uint16
 cudaError_t run_unpack(const Shape& sh, const void* src, uint32_t* planes, uint16_t* alpha, uint16_t* offset,
                        cudaStream_t st) {
   if (planes)
-    unpack_keys_kernel<<<blocks_for((size_t)sh.q * sh.m * (sh.n / 32)), kPackThreads, 0, st>>>(
+    unpack_keys_kernel<<<blocks_for((size_t)sh.q * sh.m * ((sh.n + 31) / 32)), kPackThreads, 0, st>>>(
         static_cast<const uint8_t*>(src), planes, sh);
   if (alpha || offset)
     unpack_scales_kernel<<<blocks_for((size_t)sh.m * sh.G), kPackThreads, 0, st>>>(static_cast<const uint8_t*>(src),

@@ -188,8 +188,8 @@ def lutgemm_pack_uniform(codes: torch.Tensor, scale: torch.Tensor, zero: torch.T
 def lutgemm_unpack_bcq(w: PackedBCQ, stream=None):
     """Native -> canonical (planes int32 [q][m][n/32], alpha fp16 [m][G][q], offset fp16 [m][G] | None)."""
     dev = w.data.device
-    G = w.n // w.g
-    planes = torch.empty((w.q, w.m, w.n // 32), dtype=torch.int32, device=dev)
+    G = w.n // w.g  # g divides n
+    planes = torch.empty((w.q, w.m, (w.n + 31) // 32), dtype=torch.int32, device=dev)
     alpha = torch.empty((w.m, G, w.q), dtype=torch.float16, device=dev)
     offset = torch.empty((w.m, G), dtype=torch.float16, device=dev) if w.has_offset else None
     _check("lutgemm_unpack_bcq", lib.lutgemm_unpack_bcq(ctypes.byref(w.struct), planes.data_ptr(), alpha.data_ptr(),

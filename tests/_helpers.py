@@ -29,40 +29,56 @@ def assert_parity(y_gpu, y_ref, what=""):
 
 def native_pack_reference(planes: np.ndarray, alpha: np.ndarray, offset, m: int, n: int, q: int, g: int):
     """Independent statement of layout.cuh: slice-major (1024 columns per slice,
-    L_s lanes of 32 columns); slice s = three regions, each zero-padded to a
-    multiple of 256 bytes: keys [RQ][q][L_s][4 rows] uint32, alpha
-    [RQ][gps][q][4 rows] fp16, z [RQ][gps][4 rows] fp16 (if offset);
-    gps = 32 L_s / g (g <= 1024) else 1."""
+    L_s lanes of 32 columns, the last lane possibly partial); slice s = three
+    regions, each zero-padded to a multiple of 256 bytes: keys [RQ][q][L_s][4 rows]
+    uint32, alpha [RQ][gps][q][4 rows] fp16, z [RQ][gps][4 rows] fp16 (if offset).
+    Scale entries per slice (gps) by group class:
+      g == n or a multiple of 1024: 1 entry, the group holding the slice's first column;
+      g | 1024 (g % 32 == 0): 32 L_s / g groups;
+      other g % 32 == 0: (g + 991) // g + 1 entries, groups floor(1024 s / g) + k
+        (entries past the last group are zero);
+      g % 32 != 0 (chunk groups): alpha [RQ][L_s][q][4 chunks][4 rows] and
+        z [RQ][L_s][4 chunks][4 rows], entry (lane p, chunk j) = group of column
+        1024 s + 32 p + 8 j (zero past n)."""
     m4 = (m + 3) // 4 * 4
     RQ = m4 // 4
     G = n // g
-    nw = n // 32
+    nw = (n + 31) // 32
     P = np.zeros((q, m4, nw), dtype=np.uint32)
     P[:, :m] = planes
-    A = np.zeros((m4, G, q), dtype=np.float16)
-    A[:m] = alpha
-    Z = np.zeros((m4, G), dtype=np.float16)
+    A = np.zeros((m4, G + 1, q), dtype=np.float16)   # group index G = the zero entry
+    A[:m, :G] = alpha
+    Z = np.zeros((m4, G + 1), dtype=np.float16)
     if offset is not None:
-        Z[:m] = offset
+        Z[:m, :G] = offset
 
     def pad256(b):
         return np.concatenate([b, np.zeros((-len(b)) % 256, np.uint8)])
 
+    chunk = g % 32 != 0 and g != n
     out = []
     for s in range((n + 1023) // 1024):
         w0, w1 = 32 * s, min(nw, 32 * s + 32)
         L = w1 - w0
-        if g <= 1024:
-            gps = 32 * L // g
-            grps = list(range(s * (1024 // g), s * (1024 // g) + gps))
-        else:
-            gps, grps = 1, [(s * 1024) // g]
         keys = P[:, :, w0:w1].reshape(q, RQ, 4, L).transpose(1, 0, 3, 2)          # [RQ][q][L][4]
-        al = A[:, grps, :].reshape(RQ, 4, gps, q).transpose(0, 2, 3, 1)           # [RQ][gps][q][4]
         out.append(pad256(np.ascontiguousarray(keys).view(np.uint8).reshape(-1)))
+        if chunk:
+            cols = 1024 * s + 32 * np.arange(L)[:, None] + 8 * np.arange(4)[None, :]  # [L][4]
+            grp = np.where(cols < n, cols // g, G)
+            al = A[:, grp.reshape(-1), :].reshape(RQ, 4, L, 4, q).transpose(0, 2, 4, 3, 1)  # [RQ][L][q][4][4]
+            zz = Z[:, grp.reshape(-1)].reshape(RQ, 4, L, 4).transpose(0, 2, 3, 1)           # [RQ][L][4][4]
+        else:
+            if g == n or (g >= 1024 and g % 1024 == 0):
+                grps = [(s * 1024) // g]
+            elif 1024 % g == 0:
+                grps = list(range(s * (1024 // g), s * (1024 // g) + 32 * L // g))
+            else:
+                grps = [min(G, (s * 1024) // g + k) for k in range((g + 991) // g + 1)]
+            gps = len(grps)
+            al = A[:, grps, :].reshape(RQ, 4, gps, q).transpose(0, 2, 3, 1)       # [RQ][gps][q][4]
+            zz = Z[:, grps].reshape(RQ, 4, gps).transpose(0, 2, 1)                 # [RQ][gps][4]
         out.append(pad256(np.ascontiguousarray(al).view(np.uint8).reshape(-1)))
         if offset is not None:
-            zz = Z[:, grps].reshape(RQ, 4, gps).transpose(0, 2, 1)                 # [RQ][gps][4]
             out.append(pad256(np.ascontiguousarray(zz).view(np.uint8).reshape(-1)))
     return np.concatenate(out)
 

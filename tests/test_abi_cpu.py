@@ -69,15 +69,39 @@ def test_abi_version_and_sizes():
     assert L.lutgemm_workspace_bytes(49152, 12288, 8) == 2304 + 12 * 8 * 49152 * 4
 
 
-@pytest.mark.parametrize("m,n,q,g", [(0, 64, 3, 32), (8, 48, 3, 48), (8, 64, 0, 32), (8, 64, 9, 32),
-                                     (8, 64, 3, 16), (8, 96, 3, 64), (8, 64, 3, 96), (8, 192, 3, 96),
-                                     (8, 6144, 3, 1536)])
+@pytest.mark.parametrize("m,n,q,g", [(0, 64, 3, 32), (8, 64, 0, 32), (8, 64, 9, 32), (8, 96, 3, 64),
+                                     (8, 64, 3, 96), (8, 44, 3, 44), (8, 96, 3, 12), (8, 64, 3, 0),
+                                     (8, 4, 3, 4), (8, 4104, 3, 32)])
 def test_invalid_shapes_rejected(m, n, q, g):
     import paper_2206_09557_b200 as L
     with pytest.raises(L.LutgemmError) as ei:
         L.lutgemm_packed_bytes(m, n, q, g, False)
     assert ei.value.status == 1
     assert "must" in str(ei.value)
+
+
+@pytest.mark.parametrize("m,n,q,g,off", [(5, 48, 3, 48, False), (8, 64, 3, 16, True), (8, 192, 3, 96, False),
+                                         (3, 6144, 3, 1536, True), (9, 4800, 3, 96, True), (6, 4608, 2, 384, False),
+                                         (7, 4104, 3, 24, True), (10, 1000, 2, 8, False), (3, 4104, 4, 4104, True),
+                                         (4, 12288, 3, 128, False), (2, 2040, 5, 40, True)])
+def test_general_shapes_accepted_and_sized(m, n, q, g, off):
+    """SURVEY 8(b)'s shape contract (n % 8, g % 8, g | n): accepted, and the library's packed size
+    equals the independent numpy statement of the layout (tests/_helpers.native_pack_reference)."""
+    import numpy as np
+    import paper_2206_09557_b200 as L
+    from tests._helpers import native_pack_reference
+    from workloads import gen_bcq
+    d = gen_bcq(1, m, n, q, g, offset=off)
+    ref = native_pack_reference(d["planes"], d["alpha"], d["offset"], m, n, q, g)
+    assert L.lutgemm_packed_bytes(m, n, q, g, off) == len(ref)
+
+
+def test_compact_format_needs_whole_lane_groups():
+    import paper_2206_09557_b200 as L
+    assert L.lutgemm_packed_bytes(8, 4800, 3, 96, True, L.FMT_UNIFORM_COMPACT) > 0
+    with pytest.raises(L.LutgemmError) as ei:
+        L.lutgemm_packed_bytes(8, 4104, 3, 24, True, L.FMT_UNIFORM_COMPACT)
+    assert ei.value.status == 1 and "compact" in str(ei.value)
 
 
 def test_gemv_argument_validation_without_gpu():
