@@ -213,10 +213,10 @@ lutgemm_status lutgemm_gemm_host(const lutgemm_weight* w, const uint16_t* X_host
 /* Tracing (debug; not for the hot path).  Enabling clears the buffer; then every subsequent
  * product launch records a per-CTA %globaltimer timeline into a library-owned
  * device buffer (8 u64 per CTA, up to 1024 CTAs, last launch wins):
- * [0] CTA start, [1] x slice staged, [2] first LUT built, [3] warp 0 done with
- * the first segment, [4] all warps done with it, [5] PDL wait done (fused
- * GEMV: overwritten by "row group complete" in reducer CTAs), [6] CTA end
- * (reduction share done), [7] SM id (high word: segments processed).  lutgemm_trace_read copies up to
+ * [0] CTA start, [1] x slice in hand (registers or staged), [2] first LUT built,
+ * [3] PDL wait done, [4] all warps done with the first segment, [5] row group
+ * complete (fused GEMV reducer CTAs), [6] CTA end (reduction share done),
+ * [7] SM id (high word: segments processed).  lutgemm_trace_read copies up to
  * n values to host memory (synchronous) and returns how many it copied. */
 lutgemm_status lutgemm_trace_enable(int on);
 size_t lutgemm_trace_read(uint64_t* host, size_t n);

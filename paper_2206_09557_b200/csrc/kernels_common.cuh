@@ -20,11 +20,10 @@ constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMiscBytes = 8192;       // x double buffer (2 x 2 KB) + mbarriers + flags
 // dynamic shared memory per CTA: the LUT (128 KB) on a 64 KB boundary + misc for any base alignment.
-// The opt-in maximum (227 KB) includes static shared memory; the product kernels declare none
-// (tests/test_abi_cpu.py checks the SASS resource usage).  A 227 KB variant with a weight prefetch
-// area before the PDL wait measured slower everywhere (measured and dropped).
-constexpr int kSmemBytes = 227 * 1024;     // the attribute set on every product kernel (upper bound)
-constexpr int kSmemBytesBase = 3 * 65536;  // what the launches request
+// The product kernels declare no static shared memory (tests/test_abi_cpu.py checks the SASS
+// resource usage).  A 227 KB variant with a weight prefetch area before the PDL wait measured slower
+// everywhere (measured and dropped): the larger carveout takes L1 capacity.
+constexpr int kSmemBytesBase = 3 * 65536;
 constexpr int kMiscArrive = 4128;      // misc-block offset of the fused reduction's arrival slot (u32)
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kFusedMaxJ = 256;        // max CTAs per slice in the fused-reduction mode
@@ -52,8 +51,7 @@ __device__ __forceinline__ uint32_t table_offset(int l, int j) {
 // Build entries [64h, 64h+64) of one table T[k] = sum_j (2 bit_j(k) - 1) x_j
 // (mu = 8, key bit j <-> column 8t+j, R3).  T[k] = L[k&15] + H[k>>4]
 // with L over x0..x3 and H over x4..x7: one add per entry (Eq. 2's C_build).
-__device__ __forceinline__ void build_table_part(uint32_t tbl, const __half* xc, int h) {
-  const uint4 raw = *reinterpret_cast<const uint4*>(xc);
+__device__ __forceinline__ void build_table_part(uint32_t tbl, uint4 raw, int h) {
   const float2 x01 = h2_to_f2(raw.x), x23 = h2_to_f2(raw.y), x45 = h2_to_f2(raw.z), x67 = h2_to_f2(raw.w);
   const float a[4] = {-x01.x - x01.y, x01.x - x01.y, -x01.x + x01.y, x01.x + x01.y};
   const float b[4] = {-x23.x - x23.y, x23.x - x23.y, -x23.x + x23.y, x23.x + x23.y};
@@ -149,9 +147,22 @@ struct LaneAddr {
   uint32_t kstride;     // bytes between planes of the key block (Ls * 16)
 };
 
-__device__ __forceinline__ LaneAddr lane_addr(const Shape& sh, const uint8_t* data, int s, int Ls, int lay) {
+__device__ __forceinline__ LaneAddr lane_addr(const Shape& sh, const FullSlice& fs, const uint8_t* data, int s,
+                                              int Ls, int lay) {
   LaneAddr a;
   const int k = lane_group(sh, s, lay);
+  if (Ls == kLanesPerSlice) {  // full slice: host-computed constants (layout.cuh's formulas)
+    const uint8_t* base = data + (size_t)s * fs.stride;
+    const uint32_t qa = (uint32_t)scale_planes(sh);
+    a.kp = base + (uint32_t)lay * 16u;
+    a.ap = base + fs.aoff + (sh.gcls == kGrpChunk ? (uint32_t)lay * qa * 32u : (uint32_t)k * qa * 8u);
+    a.zp = base + fs.zoff + (uint32_t)k * 8u;
+    a.KB = fs.KB;
+    a.AB = fs.AB;
+    a.ZB = fs.ZB;
+    a.kstride = kLanesPerSlice * 16u;
+    return a;
+  }
   a.kp = data + key_at(sh, s, Ls, 0, 0, lay, 0);
   a.ap = data + alpha_at(sh, s, Ls, 0, 0, k, 0);
   a.zp = data + z_at(sh, s, Ls, 0, k, 0);

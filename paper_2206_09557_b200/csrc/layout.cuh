@@ -52,6 +52,7 @@ struct Shape {
   int m, n, q, g, has_z;
   int compact;  // 1: uniform-compact format (one stored scale s per group, has_z = 1)
   int gcls;     // group class: kGrpOne (row-wise / multiple of 1024), kGrpDiv (g | 1024), kGrpSpan, kGrpChunk
+  int lsh;      // kGrpDiv: log2(g / 32), a layout lane's group is p >> lsh (g / 32 is a power of two)
   int m4, RQ, G, S;
 };
 
@@ -67,6 +68,8 @@ __host__ __device__ inline Shape make_shape(int m, int n, int q, int g, int has_
   s.m = m; s.n = n; s.q = q; s.g = g; s.has_z = (has_z || compact) ? 1 : 0;
   s.compact = compact ? 1 : 0;
   s.gcls = group_class(n, g);
+  s.lsh = 0;
+  while (s.gcls == kGrpDiv && (32 << s.lsh) < g) ++s.lsh;
   s.m4 = (m + 3) / 4 * 4;
   s.RQ = s.m4 / 4;
   s.G = (n + g - 1) / g;
@@ -101,7 +104,7 @@ __host__ __device__ inline int slice_groups(const Shape& sh, int Ls) {
 __host__ __device__ inline int lane_group(const Shape& sh, int s, int p) {
   switch (sh.gcls) {
     case kGrpOne: return 0;
-    case kGrpDiv: return (32 * p) / sh.g;
+    case kGrpDiv: return p >> sh.lsh;
     case kGrpSpan: return (s * kSliceCols + 32 * p) / sh.g - (s * kSliceCols) / sh.g;
     default: return 4 * p;
   }

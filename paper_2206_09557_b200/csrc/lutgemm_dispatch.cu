@@ -33,7 +33,10 @@ cudaError_t ensure_smem_attr(const void* kernel) {
   std::lock_guard<std::mutex> lock(mu);
   for (const auto& d : done)
     if (d.first == kernel && d.second == dev) return cudaSuccess;
-  const cudaError_t err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  // the attribute is what the launches request (not the 227 KB opt-in maximum): the shared-memory
+  // carveout follows it, and every KB not taken from the L1 keeps load sectors in flight
+  static const int smax = getenv("LUTGEMM_SMEM_ATTR") ? atoi(getenv("LUTGEMM_SMEM_ATTR")) : kSmemBytesBase;
+  const cudaError_t err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
   if (err == cudaSuccess) done.emplace_back(kernel, dev);
   return err;
 }
@@ -90,7 +93,8 @@ size_t trace_read(unsigned long long* host, size_t n) {
 // idling at most 8 % of the SMs, and at least J row units per slice
 static bool fusable(int S, int units, int sms) {
   const int J = S <= sms ? sms / S : 0;
-  return J >= 1 && J <= kFusedMaxJ && S <= kFusedMaxJ && S * J * 100 >= sms * 92 && units >= J;
+  return J >= 1 && J <= kFusedMaxJ && S <= kFusedMaxJ && S * J * 100 >= sms * 92 && units >= J &&
+         (long long)units * J < (1LL << 31);  // the kernels' 32-bit row-group arithmetic
 }
 
 static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint16_t* x, int b, uint16_t* y, float* yf,
@@ -131,6 +135,7 @@ static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint1
   p.counters = static_cast<unsigned*>(ws);
   p.partial = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + counters_bytes(sh));
   p.sh = sh;
+  p.fs = full_slice(sh);
   p.b = b;
   int bl = 0;
   while ((1 << bl) < batch_pad(b)) ++bl;
@@ -178,6 +183,10 @@ static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint1
   }
   p.fused_pair = pa ? 1 : 0;  // P2P epilogue: 8-row units, so row-quad groups start at even quads
   p.smem_bytes = kSmemBytesBase;
+  {
+    static const int xd = getenv("LUTGEMM_XDIRECT") ? atoi(getenv("LUTGEMM_XDIRECT")) : 1;
+    p.xdirect = xd;
+  }
   if (!batched) {
     const int sms = num_sms();
     const int J = sh.S <= sms ? sms / sh.S : 0;

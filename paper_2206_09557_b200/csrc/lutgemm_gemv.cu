@@ -46,9 +46,10 @@ namespace lg {
 // ---------------------------------------------------------------------------
 // first row quad of row-quad group fj of J (fused mode); with `pair` (P2P epilogue) groups start
 // on even quads, so the epilogue's 8-row units never straddle two groups
+// (32-bit arithmetic: the host runs the fused mode only when RQ * J < 2^31)
 __device__ __forceinline__ int group_quad(int RQ, int J, int fj, int pair) {
-  if (!pair) return (int)((long long)RQ * fj / J);
-  return min(RQ, 2 * (int)((long long)((RQ + 1) / 2) * fj / J));
+  if (!pair) return (int)((unsigned)RQ * (unsigned)fj / (unsigned)J);
+  return min(RQ, 2 * (int)((unsigned)((RQ + 1) / 2) * (unsigned)fj / (unsigned)J));
 }
 
 // 8 consecutive fp32 rows [r, r + 8) of the slice partials summed over the S slices in slice
@@ -232,7 +233,10 @@ __device__ __forceinline__ void p2p_epilogue(const KParams& p, int J, int R, int
   }
 }
 
-template <int QT, int ZM, int PD>
+// EP: the fused tensor-parallel epilogue (p2p_mode != 0) is compiled only into the EP = true
+// instantiations -- its code in the same function costs the plain kernel's main loop ~3 % more
+// instructions (the compiler loses the uniform loop counters) and ~2 us on fc1
+template <int QT, int ZM, int PD, bool EP>
 __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) {
   constexpr bool HAS_Z = ZM != 0, CMP = ZM == 2;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -277,13 +281,21 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
   int e = 0;
   long long it = it0;
   while (it < it1) {
-    const int s = (int)(it / sh.RQ);
-    const int rq_a = (int)(it % sh.RQ);
-    const int rq_b = (int)min((long long)sh.RQ, (long long)rq_a + (it1 - it));
+    // the segment: slice s, row quads [rq_a, rq_b) (fused mode: one segment, no 64-bit division)
+    int s, rq_a, rq_b;
+    if (J > 0) {
+      s = (int)blockIdx.x / J;
+      rq_a = (int)(it - (long long)s * sh.RQ);
+      rq_b = (int)(it1 - (long long)s * sh.RQ);
+    } else {
+      s = (int)(it / sh.RQ);
+      rq_a = (int)(it - (long long)s * sh.RQ);
+      rq_b = (int)min((long long)sh.RQ, (long long)rq_a + (it1 - it));
+    }
     const long long itn = it + (rq_b - rq_a);
     const int Ls = slice_lanes(sh.n, s);
     const bool lane_ok = lane < Ls;
-    const LaneAddr la = lane_addr(sh, p.data, s, Ls, lane_ok ? lane : 0);
+    const LaneAddr la = lane_addr(sh, p.fs, p.data, s, Ls, lane_ok ? lane : 0);
     // this warp's row quads in the segment: rq_a + warp + 16 t, t < nt
     const int nt = rq_a + warp < rq_b ? (rq_b - (rq_a + warp) + kWarps - 1) / kWarps : 0;
     // The warp's next quad to load is at (lk, lal, lz); each load advances them
@@ -329,26 +341,31 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
         for (int d = 0; d < PD; ++d) load_quad(buf[d]);
       }
       pdl_wait();
-      if (trace) trace[5] = globaltimer_ns();
-      if (warp == 0) stage_x(xbuf0, bar0, p.x, sh.n, s * kSliceCols, slice_cols(sh.n, s), 32, 1, 1, lane);
+      if (trace) trace[3] = globaltimer_ns();
+      if (warp == 0 && !p.xdirect)
+        stage_x(xbuf0, bar0, p.x, sh.n, s * kSliceCols, slice_cols(sh.n, s), 32, 1, 1, lane);
     }
+    // this thread's 8 x values of slice s for the LUT build: direct mode loads them from global
+    // memory (L2) into registers, no shared-memory staging, mbarrier or barrier on the path
+    const int xc = (4 * lane + (warp & 3)) * 8;  // column of the chunk within the slice
+    uint4 xraw = make_uint4(0, 0, 0, 0);
+    if (p.xdirect && xc < slice_cols(sh.n, s)) xraw = ldcg_u4(p.x + (size_t)s * kSliceCols + xc);
     if (e > 0 || J == 0) {
 #pragma unroll
       for (int d = 0; d < PD; ++d) load_quad(buf[d]);
     }
-    if (e == 0) __syncthreads();  // the zero-fill of the x buffer is visible
-    // 2. wait for the staged x slice and build the 128 LUTs of the slice
-    __half* xb = (e & 1) ? xbuf1 : xbuf0;
-    mbar_wait((e & 1) ? bar1 : bar0, (uint32_t)((e >> 1) & 1));
-    if (trace && e == 0) trace[1] = globaltimer_ns();
-    {
-      const int l = lane, j = warp & 3, h = warp >> 2;
-      build_table_part(sm.lut + table_offset(l, j), xb + (4 * l + j) * 8, h);
+    // 2. (bulk-copy mode) wait for the staged x slice; build the 128 LUTs of the slice
+    if (!p.xdirect) {
+      if (e == 0) __syncthreads();  // the zero-fill of the x buffer is visible
+      mbar_wait((e & 1) ? bar1 : bar0, (uint32_t)((e >> 1) & 1));
+      xraw = *reinterpret_cast<const uint4*>(((e & 1) ? xbuf1 : xbuf0) + xc);
     }
+    if (trace && e == 0) trace[1] = globaltimer_ns();
+    build_table_part(sm.lut + table_offset(lane, warp & 3), xraw, warp >> 2);
     __syncthreads();
     if (trace && e == 0) trace[2] = globaltimer_ns();
     // 3. stage the next segment's x slice into the other buffer
-    if (warp == 0 && itn < it1) {
+    if (warp == 0 && itn < it1 && !p.xdirect) {
       const int sn = (int)(itn / sh.RQ);
       stage_x((e & 1) ? xbuf0 : xbuf1, (e & 1) ? bar0 : bar1, p.x, sh.n, sn * kSliceCols,
               slice_cols(sh.n, sn), 32, 1, 1, lane);
@@ -386,7 +403,6 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
 #pragma unroll
     for (int d = 0; d < NB - 1; ++d)
       if (t0 + d < nt) quad(buf[d]);
-    if (trace && e == 0) trace[3] = globaltimer_ns();  // warp 0's loop end
     __syncthreads();  // the LUT and x buffer are reused by the next segment
     if (trace) trace[e == 0 ? 4 : 6] = globaltimer_ns();  // all warps done
     it = itn;
@@ -420,7 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     if (trace) trace[5] = globaltimer_ns();  // (re-used) the group is complete
     const int ri = k - (sh.S - R);
     const int g0 = group_quad(sh.RQ, J, fj, p.fused_pair), g1 = group_quad(sh.RQ, J, fj + 1, p.fused_pair);
-    if (p.p2p_mode == 0) {
+    if (!EP) {
       // plain output: this reducer's rows of the group, one thread per row
       const int r0 = 4 * (g0 + (int)((long long)(g1 - g0) * ri / R));
       const int r1 = min(sh.m, 4 * (g0 + (int)((long long)(g1 - g0) * (ri + 1) / R)));
@@ -504,7 +520,8 @@ struct GemvLaunch {
   static cudaError_t run(const KParams& p, int grid, cudaStream_t st) {
     // quads in flight per warp while one is computed (ring of PD + 1 buffers)
     constexpr int PD = QT <= 1 ? 6 : (QT <= 2 ? 4 : (QT <= 4 ? 2 : 1));
-    return launch(lut_gemv_kernel<QT, ZM, PD>, grid, p, st);
+    if (p.p2p_mode != 0) return launch(lut_gemv_kernel<QT, ZM, PD, true>, grid, p, st);
+    return launch(lut_gemv_kernel<QT, ZM, PD, false>, grid, p, st);
   }
 };
 

@@ -10,6 +10,26 @@
 
 namespace lg {
 
+// the layout constants of a full (32-lane) slice, computed once on the host so the kernels' prologue
+// does not re-derive them (layout.cuh)
+struct FullSlice {
+  unsigned long long stride;  // bytes per slice
+  unsigned long long aoff;    // offset of the alpha region in a slice
+  unsigned long long zoff;    // offset of the z region
+  uint32_t KB, AB, ZB;        // bytes per row quad of each region
+};
+
+__host__ __device__ inline FullSlice full_slice(const Shape& sh) {
+  FullSlice f;
+  f.KB = keys_bytes(sh, kLanesPerSlice);
+  f.AB = alpha_bytes(sh, kLanesPerSlice);
+  f.ZB = z_bytes(sh, kLanesPerSlice);
+  f.stride = slice_bytes(sh, kLanesPerSlice);
+  f.aoff = pad256((size_t)sh.RQ * f.KB);
+  f.zoff = f.aoff + pad256((size_t)sh.RQ * f.AB);
+  return f;
+}
+
 struct KParams {
   const uint8_t* data;   // packed record stream (layout.cuh)
   const __half* x;   // [b][n]
@@ -18,6 +38,7 @@ struct KParams {
   float* partial;    // [S][b][m4] split-K partials
   unsigned* counters;  // GEMV fused mode: arrive/depart counters per row-quad group (zero between launches)
   Shape sh;
+  FullSlice fs;      // full_slice(sh)
   int b;
   int bl;            // batched: log2 of the padded batch b_pad >= b (partials are [S2][m4][b_pad])
   int nv;            // batched: V-wide batch vectors per table entry slot group (b_pad = V * nv)
@@ -26,6 +47,8 @@ struct KParams {
   int fused_J;       // GEMV: CTAs per slice in the fused-reduction mode (0: separate reduction kernel)
   int fused_pair;    // GEMV fused mode: row-quad group boundaries on even quads (8-row units)
   int smem_bytes;    // dynamic shared memory per CTA (0: kSmemBytesBase)
+  int xdirect;       // GEMV: each thread loads its 8 x values for the LUT build straight from global memory
+                     // (0: the slice is staged into shared memory by the bulk-copy engine first)
   int reducers;      // GEMV fused mode: the last R CTAs to arrive in a row-quad group reduce it
   // fused tensor-parallel epilogue over peer memory (NEXT-1, lutgemm_p2p.cu).  p2p_mode 1 (rows
   // all-gather): each finished fp16 row r goes to window[par][pr] + p2p_yarea + 2 (yoff + r) of every

@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemvv_kernel(const KParams p)
     const int Ls = slice_lanes(sh.n, s);
     const int Lh = min(LR, Ls - LR * h);
     const bool lane_ok = w < Lh;
-    const LaneAddr la = lane_addr(sh, p.data, s, Ls, LR * h + (lane_ok ? w : 0));
+    const LaneAddr la = lane_addr(sh, p.fs, p.data, s, Ls, LR * h + (lane_ok ? w : 0));
     // this warp's groups ga + warp + 16 t, t < nt; the lane's quad V group + qi exists for t < ntl
     const int nt = ga + warp < gb ? (gb - (ga + warp) + kWarps - 1) / kWarps : 0;
     const int last_quad = V * (ga + warp + kWarps * (nt - 1)) + qi;

@@ -74,6 +74,13 @@ __device__ __forceinline__ uint4 ldg_stream_u4(const void* p) {
   return r;
 }
 
+// 16-byte load through L2 only (data another grid wrote: no stale L1 line can be hit)
+__device__ __forceinline__ uint4 ldcg_u4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
 __device__ __forceinline__ uint4 ldg_nc_u4(const void* p) {
   uint4 r;
   asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));

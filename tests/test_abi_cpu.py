@@ -37,9 +37,9 @@ def test_library_is_sm100a_only():
 
 
 def test_product_kernels_fit_the_shared_memory_opt_in():
-    """The product kernels request 227 KB of dynamic shared memory, the per-CTA opt-in maximum; any
-    static __shared__ variable on top (beyond the 1 KB the system reserves per CTA) makes every launch
-    fail with cudaErrorInvalidValue, so none may declare one."""
+    """The product kernels size their dynamic shared memory for the LUT; a static __shared__ variable
+    on top (beyond the 1 KB the system reserves per CTA) once pushed a 227 KB request past the per-CTA
+    opt-in maximum and every launch failed with cudaErrorInvalidValue, so none may declare one."""
     import subprocess
     import paper_2206_09557_b200.lutgemm as B
     out = subprocess.run(["cuobjdump", "-res-usage", B.LIB_PATH], capture_output=True, text=True).stdout

@@ -44,14 +44,16 @@ def one(m, n, q, g, reps=24, chain=False):
         runs.append(t)
     L.lutgemm_trace_enable(False)
     # per launch: times relative to the earliest CTA start
-    stats = {k: [] for k in ("launch_to_staged", "lut_build", "loop_med", "loop_spread", "end_spread",
-                             "group_wait", "reduce", "span")}
+    stats = {k: [] for k in ("start_skew", "start_to_pdl", "pdl_to_x", "lut_build", "loop_med", "loop_spread",
+                             "end_spread", "group_wait", "reduce", "span")}
     per_sm = {}
     for t in runs:
         t0 = t[:, 0].min()
         rel = (t[:, :7] - t0) / 1e3
         loop = rel[:, 4] - rel[:, 2]
-        stats["launch_to_staged"].append(float(np.median(rel[:, 1])))
+        stats["start_skew"].append(float(np.median(rel[:, 0])))
+        stats["start_to_pdl"].append(float(np.median(rel[:, 3] - rel[:, 0])))
+        stats["pdl_to_x"].append(float(np.median(rel[:, 1] - rel[:, 3])))
         stats["lut_build"].append(float(np.median(rel[:, 2] - rel[:, 1])))
         stats["loop_med"].append(float(np.median(loop)))
         stats["loop_spread"].append(float(loop.max() - loop.min()))
