@@ -12,9 +12,12 @@ applied, cross-slice reduction, fp16 y.  Inputs are
 resident in HBM; weights rotate over copies whose total exceeds 3x L2, so
 every step streams its weights from HBM (config.l2 says so).
 
-N > 1 (torchrun): weak scaling -- every rank owns an fc1-sized row shard of a
-(49152 N) x 12288 layer, runs its GEMV and the rows are all-gathered over
-NCCL (lutgemm_tp_linear ROWS_ALLGATHER).  Time = max over ranks.
+N > 1 (torchrun): strong scaling, tensor parallel (Table 4) --
+--tp-mode rows (default): rank r owns fc1 rows [r m/N, (r+1) m/N) and the fp16 rows are
+all-gathered; --tp-mode cols: rank r owns fc2 columns [r n/N, (r+1) n/N) and the fp32
+partials are all-reduced.  --tp-impl nccl (lutgemm_tp_linear) or p2p (the exchange fused
+into the GEMV epilogue over peer memory, lutgemm_p2p_*).  value = whole-layer bytes / step
+time (max over ranks); the line adds per-GPU GB/s, the shard GEMV time and the exchange time.
 
 --impl reference times the CPU fp64 oracle (the only reference this paper
 has; there is no released code) on rank 0 over a bounded row sample.

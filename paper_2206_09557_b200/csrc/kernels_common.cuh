@@ -26,7 +26,6 @@ constexpr int kMiscBytes = 8192;       // x double buffer (2 x 2 KB) + mbarriers
 constexpr int kSmemBytesBase = 3 * 65536;
 constexpr int kMiscArrive = 4128;      // misc-block offset of the fused reduction's arrival slot (u32)
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kFusedMaxJ = 256;        // max CTAs per slice in the fused-reduction mode
 
 struct SmemMap {
   uint32_t lut;     // shared-window address of the LUT (multiple of 64 KB)
@@ -607,6 +606,14 @@ inline cudaError_t launch(K kernel, int grid, const KParams& p, cudaStream_t st,
   cfg.attrs = const_cast<cudaLaunchAttribute*>(pdl_attr());
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, p);
+}
+
+// fused mode: CTA c -> (slice or sub-slice c / J, row group c % J); (c + 0.5) / J in fp32 is exact
+// enough to floor correctly for any grid of the fused mode (c < 2^16, J <= 256)
+__device__ __forceinline__ void fused_slot(const KParams& p, int& s, int& fj) {
+  const int c = (int)blockIdx.x;
+  s = (int)(((float)c + 0.5f) * p.rcp_J);
+  fj = c - s * p.fused_J;
 }
 
 // per-kernel-family launchers (dispatch on q and the scale format ZM)

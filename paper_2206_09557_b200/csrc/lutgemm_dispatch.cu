@@ -53,7 +53,7 @@ const cudaLaunchAttribute* pdl_attr() {
 
 std::atomic<unsigned long long> g_launches{0};
 
-// arrival / departure counter pairs of the fused reduction, then the grid-wide
+// arrival counters and epochs of the fused reduction, then the grid-wide
 // done counter of the fused rows all-gather (256-byte aligned)
 static size_t counters_bytes(const Shape&) { return 2u * kFusedMaxJ * 4u + 256u; }
 
@@ -177,11 +177,12 @@ static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint1
     if (fusable(p.s2, NG, sms)) {
       p.fused_J = J;
       grid = p.s2 * J;
+      for (int fj = 0; fj <= J; ++fj) p.gq[fj] = (int)((long long)NG * fj / J);
+      p.rcp_J = 1.0f / (float)J;
       const long long red_bytes = (long long)p.s2 * b * 4 * (4 * V) * ((NG + J - 1) / J);
       p.reducers = (int)std::min<long long>(p.s2, (red_bytes + 16383) / 16384);
     }
   }
-  p.fused_pair = pa ? 1 : 0;  // P2P epilogue: 8-row units, so row-quad groups start at even quads
   p.smem_bytes = kSmemBytesBase;
   {
     static const int xd = getenv("LUTGEMM_XDIRECT") ? atoi(getenv("LUTGEMM_XDIRECT")) : 1;
@@ -193,6 +194,11 @@ static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint1
     if (fusable(sh.S, pa ? (sh.RQ + 1) / 2 : sh.RQ, sms)) {
       p.fused_J = J;
       grid = sh.S * J;
+      // row-quad groups; with the P2P epilogue they start on even quads (its 8-row units)
+      for (int fj = 0; fj <= J; ++fj)
+        p.gq[fj] = !pa ? (int)((long long)sh.RQ * fj / J)
+                       : std::min(sh.RQ, 2 * (int)((long long)((sh.RQ + 1) / 2) * fj / J));
+      p.rcp_J = 1.0f / (float)J;
       const long long red_bytes = (long long)sh.S * 16 * ((sh.RQ + J - 1) / J);
       p.reducers = (int)std::min<long long>(sh.S, (red_bytes + 16383) / 16384);
       const char* env = getenv("LUTGEMM_GEMV_REDUCERS");

@@ -44,14 +44,6 @@ namespace lg {
 // most a few slices), and lut_reduce_kernel follows.  Inside a segment the 16
 // warps take row quads rq_a + warp + 16 t round-robin.
 // ---------------------------------------------------------------------------
-// first row quad of row-quad group fj of J (fused mode); with `pair` (P2P epilogue) groups start
-// on even quads, so the epilogue's 8-row units never straddle two groups
-// (32-bit arithmetic: the host runs the fused mode only when RQ * J < 2^31)
-__device__ __forceinline__ int group_quad(int RQ, int J, int fj, int pair) {
-  if (!pair) return (int)((unsigned)RQ * (unsigned)fj / (unsigned)J);
-  return min(RQ, 2 * (int)((unsigned)((RQ + 1) / 2) * (unsigned)fj / (unsigned)J));
-}
-
 // 8 consecutive fp32 rows [r, r + 8) of the slice partials summed over the S slices in slice
 // order (R11); rows >= m4 read as 0
 __device__ __forceinline__ void sum8_rows(const float* partial, int S, int m4, int r, float (&v)[8]) {
@@ -247,10 +239,11 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
   const bool cg = QT == 8 && sh.gcls == kGrpChunk;  // per-chunk scales (ring_compute_cg)
   const int J = p.fused_J;
   long long it0, it1;
+  int fs = 0, fj = 0;  // fused mode: this CTA's slice and row group
   if (J > 0) {
-    const int fs = blockIdx.x / J, fj = blockIdx.x % J;
-    it0 = (long long)fs * sh.RQ + group_quad(sh.RQ, J, fj, p.fused_pair);
-    it1 = (long long)fs * sh.RQ + group_quad(sh.RQ, J, fj + 1, p.fused_pair);
+    fused_slot(p, fs, fj);
+    it0 = (long long)fs * sh.RQ + p.gq[fj];
+    it1 = (long long)fs * sh.RQ + p.gq[fj + 1];
   } else {
     it0 = p.items * blockIdx.x / gridDim.x;
     it1 = p.items * (blockIdx.x + 1) / gridDim.x;
@@ -284,9 +277,9 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     // the segment: slice s, row quads [rq_a, rq_b) (fused mode: one segment, no 64-bit division)
     int s, rq_a, rq_b;
     if (J > 0) {
-      s = (int)blockIdx.x / J;
-      rq_a = (int)(it - (long long)s * sh.RQ);
-      rq_b = (int)(it1 - (long long)s * sh.RQ);
+      s = fs;
+      rq_a = p.gq[fj];
+      rq_b = p.gq[fj + 1];
     } else {
       s = (int)(it / sh.RQ);
       rq_a = (int)(it - (long long)s * sh.RQ);
@@ -416,26 +409,27 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     // and each sums 1/R of its rows over the S slices in slice order
     // (deterministic, R11).  R = p.reducers (1 <= R <= S).
     unsigned& s_k = *reinterpret_cast<unsigned*>(sm.misc_p + kMiscArrive);  // no static shared memory
-    const int fj = blockIdx.x % J;
     const int R = max(1, min(p.reducers, sh.S));
+    // Arrival: a wrapping counter (atom.inc, back to 0 after the S-th arrival: no reset step, no
+    // departure atomic on the way out).  Release: the CTA's partial stores (ordered before by the
+    // barrier) are visible to whoever acquires the count.
     unsigned* arrive = p.counters + fj;
-    unsigned* depart = p.counters + kFusedMaxJ + fj;
     __syncthreads();  // all partial stores of this CTA are issued
     if (tid == 0) {
-      // release: the CTA's partial stores (ordered before by the barrier) are
-      // visible to whoever acquires the count; acquire: the last arriver sees all
-      s_k = atom_add_acq_rel_u32(arrive, 1u);
+      // wrapping arrival counter: k = arrivals before this one; it returns to 0 with the S-th, so a
+      // reducer that is not last waits until the counter falls to <= k (acquire: synchronizes with
+      // the last arriver's RMW, which acquired every earlier arrival's partial stores)
+      const unsigned kk = atom_inc_acq_rel_u32(arrive, (unsigned)sh.S - 1u);
+      if (kk >= (unsigned)(sh.S - R) && kk != (unsigned)sh.S - 1u)
+        while (ld_acquire_u32(arrive) > kk) __nanosleep(32);
+      s_k = kk;
     }
     __syncthreads();
     const int k = (int)s_k;
     if (k < sh.S - R) return;
-    if (tid == 0 && k != sh.S - 1) {
-      while (ld_acquire_u32(arrive) < (unsigned)sh.S) __nanosleep(32);
-    }
-    __syncthreads();
     if (trace) trace[5] = globaltimer_ns();  // (re-used) the group is complete
     const int ri = k - (sh.S - R);
-    const int g0 = group_quad(sh.RQ, J, fj, p.fused_pair), g1 = group_quad(sh.RQ, J, fj + 1, p.fused_pair);
+    const int g0 = p.gq[fj], g1 = p.gq[fj + 1];
     if (!EP) {
       // plain output: this reducer's rows of the group, one thread per row
       const int r0 = 4 * (g0 + (int)((long long)(g1 - g0) * ri / R));
@@ -454,17 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
         if (p.yf) p.yf[r] = v;
         else p.y[r] = __float2half_rn(v);
       }
-      __syncthreads();
-      if (tid == 0 && atomicAdd(depart, 1u) == (unsigned)R - 1) {  // the last reducer resets the pair
-        *arrive = 0u;
-        *depart = 0u;
-      }
     } else {
-      __syncthreads();  // every CTA of the group has read its arrival count before the reset below
-      if (tid == 0 && atomicAdd(depart, 1u) == (unsigned)R - 1) {
-        *arrive = 0u;
-        *depart = 0u;
-      }
       p2p_epilogue(p, J, R, fj, ri, g0, g1);
     }
     if (trace) trace[6] = globaltimer_ns();  // reduction share done

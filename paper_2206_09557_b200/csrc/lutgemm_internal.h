@@ -10,6 +10,8 @@
 
 namespace lg {
 
+constexpr int kFusedMaxJ = 256;  // max CTAs per slice in the fused-reduction mode
+
 // the layout constants of a full (32-lane) slice, computed once on the host so the kernels' prologue
 // does not re-derive them (layout.cuh)
 struct FullSlice {
@@ -44,8 +46,11 @@ struct KParams {
   int nv;            // batched: V-wide batch vectors per table entry slot group (b_pad = V * nv)
   int spi;           // batched: LUT slices per work item (split-K factor S2 = ceil(S / spi))
   int qpw;           // batched: row quads per work item (256 or 128)
-  int fused_J;       // GEMV: CTAs per slice in the fused-reduction mode (0: separate reduction kernel)
-  int fused_pair;    // GEMV fused mode: row-quad group boundaries on even quads (8-row units)
+  int fused_J;       // GEMV: CTAs per slice in the fused-reduction mode (0: separate reduction kernel);
+                     // CTA c runs slice c / J, row group c % J
+  float rcp_J;       // fused mode: 1 / J (fused_slot: the division without an integer divide)
+  int gq[kFusedMaxJ + 1];  // fused mode: first unit (row quad / quad group) of row group fj, gq[J] = units
+                     // (host-computed: no division in the kernels' prologue)
   int smem_bytes;    // dynamic shared memory per CTA (0: kSmemBytesBase)
   int xdirect;       // GEMV: each thread loads its 8 x values for the LUT build straight from global memory
                      // (0: the slice is staged into shared memory by the bulk-copy engine first)

@@ -20,10 +20,11 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemvv_kernel(const KParams p)
   const int SV = p.s2;                 // sub-slices
   const int J = p.fused_J;
   long long it0, it1;  // items = (sub-slice, quad group)
+  int fs = 0, fj = 0;  // fused mode: this CTA's sub-slice and quad-group range
   if (J > 0) {
-    const int fs = blockIdx.x / J, fj = blockIdx.x % J;
-    it0 = (long long)fs * NG + (long long)NG * fj / J;
-    it1 = (long long)fs * NG + (long long)NG * (fj + 1) / J;
+    fused_slot(p, fs, fj);
+    it0 = (long long)fs * NG + p.gq[fj];
+    it1 = (long long)fs * NG + p.gq[fj + 1];
   } else {
     it0 = p.items * blockIdx.x / gridDim.x;
     it1 = p.items * (blockIdx.x + 1) / gridDim.x;
@@ -150,21 +151,23 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemvv_kernel(const KParams p)
   }
   if (J > 0) {  // fused arrival-ordered reduction over the SV sub-slices (as in lut_gemv_kernel)
     unsigned& s_k = *reinterpret_cast<unsigned*>(sm.misc_p + kMiscArrive);  // no static shared memory
-    const int fj = blockIdx.x % J;
     const int R = max(1, min(p.reducers, SV));
-    unsigned* arrive = p.counters + fj;
-    unsigned* depart = p.counters + kFusedMaxJ + fj;
+    unsigned* arrive = p.counters + fj;  // wrapping arrival counter (see lut_gemv_kernel)
     __syncthreads();
-    if (tid == 0) s_k = atom_add_acq_rel_u32(arrive, 1u);
+    if (tid == 0) {
+      // wrapping arrival counter: k = arrivals before this one; it returns to 0 with the S-th, so a
+      // reducer that is not last waits until the counter falls to <= k (acquire: synchronizes with
+      // the last arriver's RMW, which acquired every earlier arrival's partial stores)
+      const unsigned kk = atom_inc_acq_rel_u32(arrive, (unsigned)SV - 1u);
+      if (kk >= (unsigned)(SV - R) && kk != (unsigned)SV - 1u)
+        while (ld_acquire_u32(arrive) > kk) __nanosleep(32);
+      s_k = kk;
+    }
     __syncthreads();
     const int k = (int)s_k;
     if (k < SV - R) return;
-    if (tid == 0 && k != SV - 1) {
-      while (ld_acquire_u32(arrive) < (unsigned)SV) __nanosleep(32);
-    }
-    __syncthreads();
     const int ri = k - (SV - R);
-    const int g0 = V * (int)((long long)NG * fj / J), g1 = min(sh.RQ, V * (int)((long long)NG * (fj + 1) / J));
+    const int g0 = V * p.gq[fj], g1 = min(sh.RQ, V * p.gq[fj + 1]);
     const int r0 = 4 * (g0 + (int)((long long)(g1 - g0) * ri / R));
     const int r1 = min(sh.m, 4 * (g0 + (int)((long long)(g1 - g0) * (ri + 1) / R)));
     const int nr = max(0, r1 - r0);
@@ -183,11 +186,6 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemvv_kernel(const KParams p)
       }
       if (p.yf) p.yf[(size_t)beta * sh.m + r] = v;
       else p.y[(size_t)beta * sh.m + r] = __float2half_rn(v);
-    }
-    __syncthreads();
-    if (tid == 0 && atomicAdd(depart, 1u) == (unsigned)R - 1) {
-      *arrive = 0u;
-      *depart = 0u;
     }
     return;
   }
