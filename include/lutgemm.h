@@ -202,10 +202,12 @@ lutgemm_status lutgemm_gemm_batched_f32(const lutgemm_weight* w, const uint16_t*
 
 /* End-to-end call with HOST activations and outputs: copies X_host [b][n]
  * (fp16, ideally pinned) to the device staging area inside ws, runs the
- * product, copies Y [b][m] back to Y_host and synchronises `stream` before
- * returning.  ws (device, 16-byte aligned) must hold
- * lutgemm_host_workspace_bytes(m, n, b) bytes and be initialised like any
- * workspace.  The weight stays resident on the device. */
+ * product, delivers Y [b][m] to Y_host and synchronises `stream` before
+ * returning.  When Y_host is page-locked and device-mapped (cudaHostAlloc,
+ * torch pin_memory under UVA) the product's epilogue stores Y straight into
+ * it; otherwise Y is staged in ws and copied back.  ws (device, 16-byte
+ * aligned) must hold lutgemm_host_workspace_bytes(m, n, b) bytes and be
+ * initialised like any workspace.  The weight stays resident on the device. */
 size_t lutgemm_host_workspace_bytes(int m, int n, int b);
 lutgemm_status lutgemm_gemm_host(const lutgemm_weight* w, const uint16_t* X_host, int b, uint16_t* Y_host,
                                  void* ws, size_t ws_bytes, void* stream);

@@ -246,12 +246,27 @@ lutgemm_status lutgemm_gemm_host(const lutgemm_weight* w, const uint16_t* X_host
   uint8_t* xd = static_cast<uint8_t*>(ws) + pws;
   uint8_t* yd = xd + align256((size_t)b * w->n * 2);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // Y_host in page-locked, device-mapped memory (cudaHostAlloc / torch pin_memory under UVA): the
+  // product's epilogue stores y straight into it over the host link (coalesced warp stores), no
+  // separate device-to-host copy to launch and wait for.  x keeps its copy: every CTA of a slice
+  // reads the slice, so reading x over the link would move it J times.
+  uint16_t* y_mapped = nullptr;
+  {
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, Y_host) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
+      y_mapped = static_cast<uint16_t*>(pa.devicePointer);
+    else
+      cudaGetLastError();  // clear a query error on ordinary pageable memory
+  }
   cudaError_t e = cudaMemcpyAsync(xd, X_host, (size_t)b * w->n * 2, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync H2D");
-  st = product(w, reinterpret_cast<uint16_t*>(xd), b, reinterpret_cast<uint16_t*>(yd), nullptr, ws, pws, stream);
+  st = product(w, reinterpret_cast<uint16_t*>(xd), b, y_mapped ? y_mapped : reinterpret_cast<uint16_t*>(yd), nullptr,
+               ws, pws, stream);
   if (st != LUTGEMM_OK) return st;
-  e = cudaMemcpyAsync(Y_host, yd, (size_t)b * w->m * 2, cudaMemcpyDeviceToHost, s);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync D2H");
+  if (!y_mapped) {
+    e = cudaMemcpyAsync(Y_host, yd, (size_t)b * w->m * 2, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync D2H");
+  }
   e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
   return LUTGEMM_OK;

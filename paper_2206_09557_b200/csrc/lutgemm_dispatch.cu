@@ -92,8 +92,9 @@ size_t trace_read(unsigned long long* host, size_t n) {
 // fused mode of the GEMV-structured kernels: S slices x J CTAs with J = #SMs / S,
 // idling at most 8 % of the SMs, and at least J row units per slice
 static bool fusable(int S, int units, int sms) {
+  static const int min_pct = getenv("LUTGEMM_FUSE_MIN_PCT") ? atoi(getenv("LUTGEMM_FUSE_MIN_PCT")) : 92;
   const int J = S <= sms ? sms / S : 0;
-  return J >= 1 && J <= kFusedMaxJ && S <= kFusedMaxJ && S * J * 100 >= sms * 92 && units >= J &&
+  return J >= 1 && J <= kFusedMaxJ && S <= kFusedMaxJ && S * J * 100 >= sms * min_pct && units >= J &&
          (long long)units * J < (1LL << 31);  // the kernels' 32-bit row-group arithmetic
 }
 

@@ -249,13 +249,14 @@ def test_host_entry_point_matches_device_path():
     m, n, q, g = 4096, 4096, 3, 128
     d = gen_bcq(3, m, n, q, g)
     w = pack(d)
-    for b in (1, 4):
+    for b in (1, 2, 4, 8):
         X = gen_x(3, b, n)
         Xh = torch.from_numpy(X).pin_memory()
-        Yh = torch.empty((b, m), dtype=torch.float16).pin_memory()
-        ws = L.make_workspace(L.lutgemm_host_workspace_bytes(m, n, b), "cuda")
-        L.lutgemm_gemm_host(w, Xh, Yh, ws)
-        assert np.array_equal(Yh.float().numpy(), run(w, X).astype(np.float32))
+        # pinned Y: the epilogue writes it over the host link; pageable Y: staged and copied back
+        for Yh in (torch.empty((b, m), dtype=torch.float16).pin_memory(), torch.empty((b, m), dtype=torch.float16)):
+            ws = L.make_workspace(L.lutgemm_host_workspace_bytes(m, n, b), "cuda")
+            L.lutgemm_gemm_host(w, Xh, Yh, ws)
+            assert np.array_equal(Yh.float().numpy(), run(w, X).astype(np.float32)), (b, Yh.is_pinned())
 
 
 def test_error_paths_on_device():

@@ -9,10 +9,10 @@ for l in sys.stdin:
         d=json.loads(l); print(f\"  {d['case']:28s} {d['us']:8.3f} us  iso {d.get('iso_us', 0):8.3f}\")
     elif 'rror' in l: print(l.rstrip())"; }
 for i in 1 2; do
-  for v in ${VARIANTS:-"LUTGEMM_GRID2D=0" "LUTGEMM_GRID2D=1"}; do
+  for v in ${VARIANTS:-"X=0"}; do
     echo "== new $v $i"; env $v timeout 600 python tools/sweep.py --cases $CASES --steps 400 2>&1 | summ
   done
-  for d in ${DIRS:-_ab_head}; do
-    echo "== $d $i"; (cd $d && LUTGEMM_SMEM_PF=0 timeout 600 python tools/sweep.py --cases $CASES --steps 400 2>&1 | summ)
+  for d in ${DIRS:-}; do
+    echo "== $d $i"; (cd $d && timeout 600 python tools/sweep.py --cases $CASES --steps 400 2>&1 | summ)
   done
 done
