@@ -92,7 +92,8 @@ size_t trace_read(unsigned long long* host, size_t n) {
 // fused mode of the GEMV-structured kernels: S slices x J CTAs with J = #SMs / S,
 // idling at most 8 % of the SMs, and at least J row units per slice
 static bool fusable(int S, int units, int sms) {
-  static const int min_pct = getenv("LUTGEMM_FUSE_MIN_PCT") ? atoi(getenv("LUTGEMM_FUSE_MIN_PCT")) : 92;
+  const char* env = getenv("LUTGEMM_FUSE_MIN_PCT");  // tuning / tests (>100 disables the fused mode)
+  const int min_pct = env ? atoi(env) : 80;
   const int J = S <= sms ? sms / S : 0;
   return J >= 1 && J <= kFusedMaxJ && S <= kFusedMaxJ && S * J * 100 >= sms * min_pct && units >= J &&
          (long long)units * J < (1LL << 31);  // the kernels' 32-bit row-group arithmetic
@@ -165,7 +166,7 @@ static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint1
   }
   int grid = (int)std::min<long long>((long long)num_sms(), p.items);
   // fused mode (b = 1): whole slices per CTA group, S*J CTAs with J per slice,
-  // when that idles at most 8 % of the SMs; the reduction then runs in-kernel
+  // when that idles at most 20 % of the SMs; the reduction then runs in-kernel
   // with R reducers per row-quad group (~16 KB of partials each; the others
   // exit early).  LUTGEMM_GEMV_REDUCERS overrides R (tests, tuning).
   p.fused_J = 0;

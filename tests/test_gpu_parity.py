@@ -315,6 +315,22 @@ def test_gemv_reduction_modes(monkeypatch, reducers, m, n, q, g, off):
     assert_parity(y, O.bcq_gemv(d["planes"], d["alpha"], d["offset"], X, n, g), (m, n, q, g, reducers))
 
 
+@pytest.mark.parametrize("m,n,q,g,off", [(8192, 22016, 4, 128, True), (1500, 15360, 3, 128, False),
+                                         (999, 19456, 2, 64, False)])
+def test_fused_and_split_paths_agree(monkeypatch, m, n, q, g, off):
+    """Slice counts whose fused grid idles 8-20 % of the SMs (S = 22, 15, 19): the fused mode and the
+    split-into-148 path with its separate reduction kernel give the same fp32 result bit for bit
+    (both sum the slices in order, R11) and match the oracle."""
+    d = gen_bcq(m + n + q, m, n, q, g, offset=off)
+    X = gen_x(q + n, 1, n)
+    w = pack(d)
+    y = run(w, X, f32=True)
+    monkeypatch.setenv("LUTGEMM_FUSE_MIN_PCT", "101")
+    assert np.array_equal(run(w, X, f32=True), y)
+    monkeypatch.delenv("LUTGEMM_FUSE_MIN_PCT")
+    assert_parity(run(w, X), O.bcq_gemv(d["planes"], d["alpha"], d["offset"], X, n, g), (m, n, q, g))
+
+
 def _random_configs(k=24, seed=2206):
     """Seeded random shapes over the whole supported space: m and n tails, q 1..8, every g kind
     (32..1024 powers of two, multiples of 1024, row-wise), b 1..32, offset / compact uniform."""

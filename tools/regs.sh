@@ -1,7 +1,7 @@
 #!/bin/bash
 # per-kernel register / spill report of the product kernels (ptxas -v), demangled
 cd "$(dirname "$0")/.."
-for f in paper_2206_09557_b200/csrc/lutgemm_gemv.cu paper_2206_09557_b200/csrc/lutgemm_smallb.cu \
+for f in paper_2206_09557_b200/csrc/lutgemm_gemv.cu paper_2206_09557_b200/csrc/lutgemm_gemv_ep.cu paper_2206_09557_b200/csrc/lutgemm_smallb.cu \
          paper_2206_09557_b200/csrc/lutgemm_batched.cu; do
 nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -Xptxas -v -I include -I paper_2206_09557_b200/csrc \
   --expt-relaxed-constexpr -c "$f" -o /tmp/k.o 2>&1 |

@@ -103,7 +103,9 @@ def main():
     mem_gb = torch.cuda.memory_allocated(dev) / 1e9
 
     # activations (each rank: full x; local QKV/fc1 outputs; replicated out/fc2 outputs)
-    x0 = torch.randn(H, device=dev).to(torch.float16)
+    gx = torch.Generator(device=dev)
+    gx.manual_seed(2206)
+    x0 = torch.randn(H, device=dev, generator=gx).to(torch.float16)  # seeded: x_sha is reproducible
     x = x0.clone()
     qkv_o = torch.empty(3 * H // world, dtype=torch.float16, device=dev)
     out_o = torch.empty(H, dtype=torch.float16, device=dev)
@@ -156,6 +158,8 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t[0])
     finite = bool(torch.isfinite(x.float()).all())
+    import hashlib
+    x_sha = hashlib.sha256(x.cpu().numpy().tobytes()).hexdigest()[:16]  # the token's output (bitwise check)
 
     # per-linear breakdown on this rank (eager, events around each call of one layer)
     per = {}
@@ -206,6 +210,7 @@ def main():
         print(json.dumps({
             "config": "OPT-175B decoder linear stack (96 x QKV/out/fc1/fc2), q=3 g=128, b=1",
             "layers": args.layers, "tp": world, "tp_impl": args.tp_impl if world > 1 or p2p else None,
+            "x_sha": x_sha,
             "ms_per_token": round(ms, 4),
             "GBps_per_gpu": round(bytes_token / (ms * 1e-3) / 1e9, 1),
             "weight_bytes_per_gpu": int(bytes_token), "allreduces_per_token": 2 * args.layers if world > 1 else 0,
