@@ -278,16 +278,25 @@ def run_gpu(args, cfg) -> None:
     import torch
 
     world, rank, local = dist_env()
+    if args.same_device:  # validation of the N > 1 path on one GPU: P2P exchange through CUDA IPC, gloo plumbing
+        if args.tp_impl != "p2p":
+            raise SystemExit("--same-device needs --tp-impl p2p (NCCL refuses two ranks on one GPU)")
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     import paper_2206_09557_b200 as L
     from workloads import gen_bcq, gen_x
 
     comm = p2p = None
+    cdev = dev  # device of the tensors the process group reduces
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-        comm = L.TPComm(rank, world, device=dev)
+        if args.same_device:
+            dist.init_process_group("gloo")
+            cdev = torch.device("cpu")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+            comm = L.TPComm(rank, world, device=dev)
     mode = args.tp_mode
     m, n, q, g = cfg["m"], cfg["n"], cfg["q"], cfg["g"]
     if mode == "rows":  # m-split: rank r owns rows [r m/N, (r+1) m/N) and sees the full x
@@ -316,7 +325,7 @@ def run_gpu(args, cfg) -> None:
     stream = torch.cuda.current_stream()
     tp_mode = L.TP_ROWS_ALLGATHER if mode == "rows" else L.TP_COLS_ALLREDUCE
     if world > 1:
-        tws = L.make_workspace(comm.workspace_bytes(tp_mode, ms, ns, 1), dev)
+        tws = L.make_workspace(comm.workspace_bytes(tp_mode, ms, ns, 1), dev) if comm is not None else None
         if args.tp_impl == "p2p":
             p2p = L.P2PGroup(rank, world, rows_out=m if mode == "rows" else 0, cols_m=m if mode == "cols" else 0)
 
@@ -333,15 +342,18 @@ def run_gpu(args, cfg) -> None:
         L.lutgemm_gemv(ws_list[i % ncopies], x, y_local, ws)
 
     def barrier():
-        if world > 1:
+        if world > 1 and comm is not None:
             comm.wait(stream)  # polls NCCL for asynchronous errors instead of blocking blindly
             torch.distributed.barrier(device_ids=[local])
+        elif world > 1:
+            torch.cuda.synchronize()
+            torch.distributed.barrier()
         torch.cuda.synchronize()
 
     def max_over_ranks(vals):
         if world == 1:
             return vals
-        t = torch.tensor(vals, dtype=torch.float64, device=dev)
+        t = torch.tensor(vals, dtype=torch.float64, device=cdev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return t.tolist()
 
@@ -402,13 +414,13 @@ def run_gpu(args, cfg) -> None:
         else:  # y = sum over ranks of each shard's partial: sum the fp64 oracle partials across ranks
             part = O.bcq_gemv_rows(d["planes"], d["alpha"], None, x_host, ns, g, rows_local)[0]
             if world > 1:
-                t = torch.tensor(part, dtype=torch.float64, device=dev)
+                t = torch.tensor(part, dtype=torch.float64, device=cdev)
                 torch.distributed.all_reduce(t)
                 part = t.cpu().numpy()
             got = got_all[rows_local]
             err2, ref2 = float(np.sum((got - part) ** 2)), float(np.sum(part ** 2))
         if world > 1:
-            t = torch.tensor([err2, ref2], dtype=torch.float64, device=dev)
+            t = torch.tensor([err2, ref2], dtype=torch.float64, device=cdev)
             torch.distributed.all_reduce(t)
             err2, ref2 = float(t[0]), float(t[1])
         parity = math.sqrt(err2 / ref2)
@@ -465,6 +477,8 @@ def run_gpu(args, cfg) -> None:
                        "parallelism": (f"tp{world} {mode} split + {'all-gather' if mode == 'rows' else 'all-reduce'} "
                                        f"({args.tp_impl})" if world > 1 else "single GPU"),
                        "shard": [ms, ns],
+                       **({"same_device": "validation run: all ranks on cuda:0 (not a scaling number)"}
+                          if args.same_device else {}),
                        "l2": f"{ncopies} rotating weight copies per rank = {ncopies * Bs / 1e6:.0f} MB > 3x L2 "
                              f"({l2 / 1e6:.0f} MB)",
                        "bytes_alg_per_gemv": B},
@@ -497,7 +511,8 @@ def run_gpu(args, cfg) -> None:
     if world > 1:
         if p2p is not None:
             p2p.close()
-        comm.close()
+        if comm is not None:
+            comm.close()
         torch.distributed.destroy_process_group()
 
 
@@ -517,6 +532,8 @@ def main():
     ap.add_argument("--tp-impl", default="nccl", choices=["nccl", "p2p"],
                     help="N > 1: GEMV + NCCL collective, or the exchange fused into the GEMV epilogue over peer "
                          "memory (NEXT-1; validated with processes sharing one GPU, not yet on NVLink)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="validation only: every rank on cuda:0, gloo process group, --tp-impl p2p (CUDA IPC)")
     args = ap.parse_args()
     from workloads import CONFIGS
     if args.config is None:

@@ -42,3 +42,22 @@ def test_gpu_arm_contract():
     assert d["e2e"]["h2d_bytes_per_step"] == 2 * 12288 and d["e2e"]["d2h_bytes_per_step"] == 2 * 49152
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["parity_rel_l2_sampled"] < 2e-3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["rows", "cols"])
+def test_tp_arm_two_ranks_same_device(mode):
+    """The N > 1 (strong-scaling, tensor-parallel) arm of bench.py with 2 ranks, validated on one GPU:
+    --same-device runs both ranks on cuda:0 with the fused P2P exchange over CUDA IPC; the line keeps
+    the contract and the sampled rows of the gathered / reduced output match the oracle."""
+    import subprocess
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", "--master-port", str(29650 + (mode == "cols")), os.path.join(ROOT, "bench.py"), "--gpus", "2",
+           "--steps", "20", "--warmup", "3", "--no-cpu", "--tp-impl", "p2p", "--tp-mode", mode, "--same-device"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, (r.stdout + r.stderr)[-3000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert d["parity_rel_l2_sampled"] <= 2e-3
+    assert d["tp"]["impl"] == "p2p" and "exchange_us" in d["tp"]
+    assert d["config"]["shard"] == ([24576, 12288] if mode == "rows" else [12288, 24576])
