@@ -266,12 +266,14 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
   __half* xbuf1 = reinterpret_cast<__half*>(sm.misc_p + 2048);
   const uint32_t bar0 = sm.misc + 4096, bar1 = sm.misc + 4104;
   const uint32_t lc = (sm.lut & 0xFFFF0000u) | ((uint32_t)(4 * lane + 128) << 8) | (uint32_t)(4 * lane);
-  if (tid == 0) {
-    mbar_init(bar0, 1);
-    mbar_init(bar1, 1);
-    fence_mbar_init();
+  if (!p.xdirect) {  // the bulk-copy staging of x needs its mbarriers (direct mode: no barrier here)
+    if (tid == 0) {
+      mbar_init(bar0, 1);
+      mbar_init(bar1, 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
   }
-  __syncthreads();
 
   constexpr int NB = PD + 1;  // ring of quad buffers: the load of quad t + PD is issued before quad t is computed
   int e = 0;

@@ -202,7 +202,7 @@ static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint1
                        : std::min(sh.RQ, 2 * (int)((long long)((sh.RQ + 1) / 2) * fj / J));
       p.rcp_J = 1.0f / (float)J;
       const long long red_bytes = (long long)sh.S * 16 * ((sh.RQ + J - 1) / J);
-      p.reducers = (int)std::min<long long>(sh.S, (red_bytes + 16383) / 16384);
+      p.reducers = (int)std::min<long long>(sh.S, (red_bytes + 8191) / 8192);  // ~8 KB of partials per reducer
       const char* env = getenv("LUTGEMM_GEMV_REDUCERS");
       if (env && atoi(env) > 0) p.reducers = std::min(atoi(env), sh.S);
     }
