@@ -367,7 +367,7 @@ def run_gpu(args, cfg) -> None:
     reps = max(1, math.ceil(args.steps / G))
     steps_timed = reps * G
     n0 = L.lutgemm_launch_count()
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(local, period=float(os.environ.get("LUTGEMM_CLOCK_PERIOD_S", "0.005")))
     barrier()
     with sampler:
         total_ms, per_rep, graph = _timed_graph(step, G, reps, max(1, math.ceil(args.warmup / G)), stream)
