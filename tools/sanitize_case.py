@@ -1,6 +1,7 @@
 """Small products through every kernel path, for compute-sanitizer runs:
 GEMV (fused reductions: one reducer and many), batched V=2 / V=4, compact
-uniform format, n and m tails, fp32 output.  Checks results against the oracle."""
+uniform format, n and m tails, fp32 output, every layout group class (straddling
+groups, per-chunk scales, partial last lane).  Checks results against the oracle."""
 import os
 import sys
 
@@ -26,7 +27,11 @@ def check(y, ref, what):
 
 def main():
     for (m, n, q, g, b, off) in [(512, 512, 3, 128, 1, False), (777, 5152, 4, 32, 1, True), (6000, 4096, 3, 128, 1, False), (2049, 2048, 2, 64, 1, False),
-                                 (333, 1536, 3, 128, 2, True), (130, 5152, 3, 32, 5, False), (64, 2048, 6, 2048, 32, True)]:
+                                 (333, 1536, 3, 128, 2, True), (130, 5152, 3, 32, 5, False), (64, 2048, 6, 2048, 32, True),
+                                 # SURVEY 8(b) shapes: groups straddling slices, chunk groups (g % 32 != 0, the
+                                 # generic-q kernels' per-chunk scales), n % 32 != 0; a 15-slice fused grid
+                                 (300, 4800, 3, 96, 1, True), (257, 4104, 3, 24, 1, True), (129, 4104, 3, 24, 3, True),
+                                 (200, 2040, 2, 40, 6, False), (900, 4104, 3, 4104, 2, True), (64, 15360, 3, 128, 1, False)]:
         d = gen_bcq(m + n + b, m, n, q, g, offset=off)
         X = gen_x(m + b, b, n)
         w = L.lutgemm_pack_bcq(dev(d["planes"].view(np.int32)), dev(d["alpha"]),
