@@ -22,15 +22,15 @@
 //    128-bit loads (L1::no_allocate) through running pointers in a ring of
 //    PD + 1 register buffers (loads issued before the lookups of the quad they
 //    overtake), no predicates in the steady state;
-//  * the activation slice is staged into shared memory by the bulk-copy
-//    (TMA) engine after the programmatic-dependent-launch wait;
+//  * after the programmatic-dependent-launch wait each thread loads its 8 x
+//    values from L2 straight into registers for the LUT build (the bulk-copy
+//    staging into shared memory remains as LUTGEMM_XDIRECT=0);
 //  * lookups summed and scaled with packed f32x2 adds/FMAs (FADD2/FFMA2),
 //    two rows per instruction;
 //  * per-row partials reduced across lanes by a 6-shuffle transpose-reduce and
 //    written to an fp32 split-K workspace; the cross-slice sum runs in the same
-//    kernel (arrival-ordered, fixed slice order: deterministic);
-//  * batched (2 <= b <= 32): vector table slots of V batch rows read with
-//    LDS.128 / LDS.64 (see the batched section).
+//    kernel (arrival-ordered on a self-resetting counter, fixed slice order:
+//    deterministic).  Batched products: lutgemm_smallb.cu, lutgemm_batched.cu.
 #pragma once
 #include "kernels_common.cuh"
 
