@@ -441,20 +441,27 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
       // plain output: this reducer's rows of the group, one thread per row
       const int r0 = 4 * (g0 + (int)((long long)(g1 - g0) * ri / R));
       const int r1 = min(sh.m, 4 * (g0 + (int)((long long)(g1 - g0) * (ri + 1) / R)));
-      for (int r = r0 + tid; r < r1; r += kThreads) {
-        float v = 0.f;
-        const float* pp = p.partial + r;
-        for (int ss0 = 0; ss0 < sh.S; ss0 += 16) {  // up to 16 slices per L2 round trip
-          float t[16];
+      // sum over the S slices in slice order, up to NS slices per L2 round trip (16, or 48 for the
+      // wide layers: fc2 has S = 48; a 48-wide batch measured slower for S = 12)
+      auto reduce_rows = [&](auto ns) {
+        constexpr int NS = decltype(ns)::value;
+        for (int r = r0 + tid; r < r1; r += kThreads) {
+          float v = 0.f;
+          const float* pp = p.partial + r;
+          for (int ss0 = 0; ss0 < sh.S; ss0 += NS) {
+            float t[NS];
 #pragma unroll
-          for (int kk = 0; kk < 16; ++kk) t[kk] = (ss0 + kk < sh.S) ? __ldcg(pp + (size_t)(ss0 + kk) * sh.m4) : 0.f;
+            for (int kk = 0; kk < NS; ++kk) t[kk] = (ss0 + kk < sh.S) ? __ldcg(pp + (size_t)(ss0 + kk) * sh.m4) : 0.f;
 #pragma unroll
-          for (int kk = 0; kk < 16; ++kk)
-            if (ss0 + kk < sh.S) v += t[kk];
+            for (int kk = 0; kk < NS; ++kk)
+              if (ss0 + kk < sh.S) v += t[kk];
+          }
+          if (p.yf) p.yf[r] = v;
+          else p.y[r] = __float2half_rn(v);
         }
-        if (p.yf) p.yf[r] = v;
-        else p.y[r] = __float2half_rn(v);
-      }
+      };
+      if (sh.S <= 16) reduce_rows(std::integral_constant<int, 16>{});
+      else reduce_rows(std::integral_constant<int, 48>{});
     } else {
       p2p_epilogue(p, J, R, fj, ri, g0, g1);
     }
