@@ -271,19 +271,20 @@ int lutgemm_tp_nranks(const lutgemm_tp* tp);
  * the GEMV's epilogue over peer memory (CUDA IPC mappings over NVLink / NVSwitch), no NCCL call;
  * one process per GPU (communication limits tensor parallelism once the matmul is
  * fast).  A call is ONE kernel on `stream`: the exchange runs in the fused GEMV's epilogue, in
- * the reducer CTAs (16-byte stores, system-scope release/acquire signals):
- *  - ROWS (m-split): each finished fp16 row of this rank's shard goes to y and into every
- *    peer's exchange window; the CTAs signal every rank, wait for all P signals and copy the
- *    peers' rows from the local window into y.
+ * the reducer CTAs, one thread per output row, as LL words (8-byte stores of 4 data bytes
+ * and a 4-byte round stamp, polled by the reader: no fence or separate signal):
+ *  - ROWS (m-split): each finished fp16 row pair of this rank's shard goes to y and into every
+ *    peer's exchange window; each reducer then reads the peers' rows of its own share out of the
+ *    local window into y (every rank runs the same reducer partition).
  *  - COLS (n-split): reduce-scatter + all-gather.  Rank o owns rows [o mb, (o+1) mb),
- *    mb = 8 ceil(ceil(m/P)/8); the reducers store this rank's fp32 partial rows into the
- *    owner's window only, signal, wait; each rank sums its owned block over the P slots in rank
- *    order (deterministic, bitwise identical on every rank, within tolerance of the 1-GPU
- *    result), rounds to fp16 and stores the block into y and every peer's window, signals,
- *    waits and copies the peers' blocks into y.
+ *    mb = 8 ceil(ceil(m/P)/8); each fp32 row goes to its owner's window only; each rank sums its
+ *    owned rows over the P slots in rank order (deterministic, bitwise identical on every rank,
+ *    within tolerance of the 1-GPU result), rounds to fp16 and sends the row pairs to every
+ *    peer, which copy them into y.  Every rank must own rows ((P - 1) mb < m), else
+ *    LUTGEMM_ERR_INVALID_ARG.
  * The round number lives on the device, so calls are CUDA-graph capturable; each rank owns two
- * windows (double buffer) and 64-bit signal counters.  Every rank must make the same sequence of
- * calls on a group.  y is complete when the call's kernel completes on the stream. */
+ * windows (double buffer by round parity).  Every rank must make the same sequence of calls on
+ * a group.  y is complete when the call's kernel completes on the stream. */
 typedef struct lutgemm_p2p lutgemm_p2p;
 
 /* Bytes of one exchange window for `mode` (LUTGEMM_TP_ROWS_ALLGATHER: m = rows of the gathered

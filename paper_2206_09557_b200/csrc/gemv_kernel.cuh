@@ -46,184 +46,147 @@ namespace lg {
 // most a few slices), and lut_reduce_kernel follows.  Inside a segment the 16
 // warps take row quads rq_a + warp + 16 t round-robin.
 // ---------------------------------------------------------------------------
-// 8 consecutive fp32 rows [r, r + 8) of the slice partials summed over the S slices in slice
-// order (R11); rows >= m4 read as 0
-__device__ __forceinline__ void sum8_rows(const float* partial, int S, int m4, int r, float (&v)[8]) {
-#pragma unroll
-  for (int k = 0; k < 8; ++k) v[k] = 0.f;
-  if (r + 8 <= m4) {
-    for (int s = 0; s < S; ++s) {
-      const float4 a = __ldcg(reinterpret_cast<const float4*>(partial + (size_t)s * m4 + r));
-      const float4 b = __ldcg(reinterpret_cast<const float4*>(partial + (size_t)s * m4 + r + 4));
-      v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w;
-      v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
-    }
-  } else {
-    for (int s = 0; s < S; ++s)
-      for (int k = 0; k < 8 && r + k < m4; ++k) v[k] += __ldcg(partial + (size_t)s * m4 + r + k);
-  }
-}
-
 // ---------------------------------------------------------------------------
 // Tensor-parallel exchange fused into the GEMV epilogue (NEXT-1, lutgemm_p2p.cu).
-// Runs in the R reducer CTAs of every row-quad group (NRED = J R CTAs, all resident), after the
-// group's slice partials are complete.  Rows of 8-row units [8u, 8u + 8), 16-byte stores.
-//   rows (p2p_mode 1, m-split):  fp16 rows of this rank's shard -> this rank's y (local) and every
-//     peer's window[par] at row yoff + r; signal A; wait for the P signals A; copy the peers' rows
-//     out of the local window into y.
-//   cols (p2p_mode 2, n-split):  fp32 partial rows -> the owner's window[par] slot [self]
-//     (reduce-scatter); signal A; wait; sum the owned block over the P slots in rank order
-//     (deterministic), fp16 -> y (local) and every peer's window y-area; signal B; wait; copy the
-//     peers' blocks out of the local window into y.
-// Signals: the grid's last CTA through a phase (acq_rel counter, gpu scope) issues
-// fence.acq_rel.sys and red.release.sys.u64 on every rank's counter; waits are ld.acquire.sys by
-// thread 0 followed by a CTA barrier (the chain: stores -> bar.sync -> acq_rel RMW -> last CTA's
-// acquire -> fence.sys -> release to the peer -> the peer's acquire -> its bar.sync -> its loads).
-// The last CTA of the final phase advances the device-side round (parity of the double buffer).
+// Runs in the R reducer CTAs of every row-quad group after the group's slice partials are
+// complete; reducer (fj, ri) owns rows [r0, r1) (a share of the group's 8-row units; every rank
+// runs the same partition, so the same reducer on another rank owns the same rows), one thread
+// per row, the S slice partials summed in slice order NS per L2 round trip (R11).
+//   rows (p2p_mode 1, m-split): y[yoff + r] locally; (r, r+1) as one half2 LL word into every
+//     peer's window; then the peers' rows r of their shards out of the local window into y.
+//   cols (p2p_mode 2, n-split): reduce-scatter + all-gather.  The fp32 row sum goes as an LL
+//     word to the owner o = r / mb, slot [self]; on the owner the same reducer share sums its
+//     owned rows over the P slots in rank order (deterministic, identical on every rank), rounds
+//     to fp16 and sends (r, r+1) half2 LL words to every peer; the other owners' rows are read
+//     out of the local window.
+// LL ("low-latency") words: 8 bytes = data | stamp << 32, written and read as ONE aligned 64-bit
+// access (single-copy atomic), so a reader that sees the round's stamp sees the data -- no fence,
+// no separate signal, no barrier on the path (the protocol NCCL uses for small messages).
+// stamp = low 32 bits of round + 1; the window is double-buffered by round parity, so a stale
+// word of the same parity carries stamp - 2.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint4 pack_half8(const float (&v)[8]) {
-  uint4 h;
-  h.x = pack_half2(v[0], v[1]);
-  h.y = pack_half2(v[2], v[3]);
-  h.z = pack_half2(v[4], v[5]);
-  h.w = pack_half2(v[6], v[7]);
-  return h;
+__device__ __forceinline__ void st_ll(uint8_t* p, uint32_t d, uint32_t stamp) {
+  const unsigned long long w = ((unsigned long long)stamp << 32) | d;
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
 }
-
-// store `cnt` (<= 8) fp16 values of h at dst (16-byte store when whole)
-__device__ __forceinline__ void store_half8(uint8_t* dst, const uint4& h, int cnt) {
-  if (cnt >= 8) {
-    *reinterpret_cast<uint4*>(dst) = h;
-  } else {
-    const uint16_t* hs = reinterpret_cast<const uint16_t*>(&h);
-    for (int k = 0; k < cnt; ++k) reinterpret_cast<uint16_t*>(dst)[k] = hs[k];
+__device__ __forceinline__ uint32_t ld_ll(const uint8_t* p, uint32_t stamp) {
+  unsigned long long w;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+  while ((uint32_t)(w >> 32) != stamp) {
+    __nanosleep(16);
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
   }
+  return (uint32_t)w;
 }
 
-// grid-wide phase barrier of the NRED reducer CTAs: the last to arrive (resetting the counter)
-// runs `last` in thread 0; then every CTA waits until its own signal counter reaches `target`
-template <typename F>
-__device__ __forceinline__ void p2p_phase(unsigned* cnt, unsigned nred, const unsigned long long* my_sig,
-                                          unsigned long long target, F last) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (atom_add_acq_rel_u32(cnt, 1u) == nred - 1) {
-      *cnt = 0u;
-      last();
-    }
-    while (ld_acquire_sys_u64(my_sig) < target) __nanosleep(32);
-  }
-  __syncthreads();
-}
-
-// copy units [u0, u1) of 8 fp16 rows from src to dst (both indexed from row 0), rows < rows_end
-__device__ __forceinline__ void copy_rows(__half* dst, const uint8_t* src, int u0, int u1, int rows_end) {
-  for (int u = u0 + (int)threadIdx.x; u < u1; u += kThreads) {
-    const int r = 8 * u;
-    const uint4 v = __ldcg(reinterpret_cast<const uint4*>(src) + u);
-    store_half8(reinterpret_cast<uint8_t*>(dst + r), v, rows_end - r);
-  }
-}
-
-__device__ __forceinline__ void p2p_epilogue(const KParams& p, int J, int R, int fj, int ri, int g0, int g1) {
-  const Shape& sh = p.sh;
-  const int P = p.npeers, self = p.p2p_self;
-  const unsigned nred = (unsigned)(J * R);
-  const int red = fj * R + ri;  // this CTA's index among the reducers
-  unsigned* cnt = p.counters + 2 * kFusedMaxJ;  // 3 phase counters
-  const unsigned long long round = ld_acquire_u64(p.p2p_round);  // previous round complete (PDL wait)
-  const int par = (int)(round & 1ull);
-  const unsigned long long target = (round + 1ull) * (unsigned long long)P;
-  unsigned long long* const* sig = p.p2p_sig;  // sig[pr][0] = A, [1] = B, [2] = round (self only)
-  auto signal_all = [&](int which) {
-    fence_acq_rel_sys();
-    for (int pr = 0; pr < P; ++pr) red_release_sys_add_u64(sig[pr] + which, 1ull);
-  };
-  const int u0g = g0 / 2, u1g = (g1 + 1) / 2;  // the group's 8-row units (groups start on even quads)
-  const int u0 = u0g + (int)((long long)(u1g - u0g) * ri / R), u1 = u0g + (int)((long long)(u1g - u0g) * (ri + 1) / R);
-  auto share = [&](int units, int& a, int& b) {  // this reducer's share of `units` work units
-    a = (int)((long long)units * red / nred);
-    b = (int)((long long)units * (red + 1) / nred);
-  };
-  if (p.p2p_mode == 1) {
-    const int ms = sh.m;
-    for (int u = u0 + (int)threadIdx.x; u < u1; u += kThreads) {
-      const int r = 8 * u;
-      float v[8];
-      sum8_rows(p.partial, sh.S, sh.m4, r, v);
-      const uint4 h = pack_half8(v);
-      store_half8(reinterpret_cast<uint8_t*>(p.y + p.yoff + r), h, ms - r);
-      const size_t off = 2 * (size_t)(p.yoff + r);
-      for (int pr = 0; pr < P; ++pr)
-        if (pr != self) store_half8(p.p2p_win[par][pr] + off, h, ms - r);
-    }
-    p2p_phase(cnt, nred, sig[self], target, [&] { signal_all(0); });
-    // the peers' rows: (P - 1) ms rows out of the local window
-    const int upr = ms / 8;  // ms % 8 == 0 (checked on the host)
-    int a, b;
-    share((P - 1) * upr, a, b);
-    for (int w = a + (int)threadIdx.x; w < b; w += kThreads) {
-      const int k = w / upr, pr = k + (k >= self ? 1 : 0), u = pr * upr + w % upr;
-      const uint4 v = __ldcg(reinterpret_cast<const uint4*>(p.p2p_win[par][self]) + u);
-      *reinterpret_cast<uint4*>(p.y + 8 * u) = v;
-    }
-  } else {
-    const int m = sh.m, mb = p.p2p_mb;
-    for (int u = u0 + (int)threadIdx.x; u < u1; u += kThreads) {
-      const int r = 8 * u;
-      float v[8];
-      sum8_rows(p.partial, sh.S, sh.m4, r, v);
-      const int o = r / mb;
-      float* dst = reinterpret_cast<float*>(p.p2p_win[par][o]) + (size_t)self * mb + (r - o * mb);
-      if (r + 8 <= m) {
-        reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
-        reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
-      } else {
-        for (int k = 0; k < m - r; ++k) dst[k] = v[k];
-      }
-    }
-    p2p_phase(cnt, nred, sig[self], target, [&] { signal_all(0); });
-    // owned block [self mb, self mb + mb): sum the P slots in rank order, fp16 -> y and every peer
-    const float* slots = reinterpret_cast<const float*>(p.p2p_win[par][self]);
-    const int b0 = self * mb, rows = max(0, min(mb, m - b0));
-    int a, b;
-    share((rows + 7) / 8, a, b);
-    for (int w = a + (int)threadIdx.x; w < b; w += kThreads) {
-      const int lr = 8 * w;
-      float v[8];
+// row r of the result: the S slice partials summed in slice order, NS per L2 round trip
+template <int NS>
+__device__ __forceinline__ float row_sum(const KParams& p, int r) {
+  float v = 0.f;
+  const float* pp = p.partial + r;
+  for (int ss0 = 0; ss0 < p.sh.S; ss0 += NS) {
+    float t[NS];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = 0.f;
-      for (int pr = 0; pr < P; ++pr) {
-        const float4 x0 = __ldcg(reinterpret_cast<const float4*>(slots + (size_t)pr * mb + lr));
-        const float4 x1 = __ldcg(reinterpret_cast<const float4*>(slots + (size_t)pr * mb + lr + 4));
-        v[0] += x0.x; v[1] += x0.y; v[2] += x0.z; v[3] += x0.w;
-        v[4] += x1.x; v[5] += x1.y; v[6] += x1.z; v[7] += x1.w;
-      }
-      const uint4 h = pack_half8(v);
-      store_half8(reinterpret_cast<uint8_t*>(p.y + b0 + lr), h, rows - lr);
-      const size_t off = p.p2p_yarea + 2 * (size_t)(b0 + lr);
-      for (int pr = 0; pr < P; ++pr)
-        if (pr != self) store_half8(p.p2p_win[par][pr] + off, h, rows - lr);
-    }
-    if (P > 1) {
-      p2p_phase(cnt + 1, nred, sig[self] + 1, target, [&] { signal_all(1); });
-      // the peers' blocks out of the local window
-      const int ub = mb / 8;
-      share((P - 1) * ub, a, b);
-      for (int w = a + (int)threadIdx.x; w < b; w += kThreads) {
-        const int k = w / ub, pr = k + (k >= self ? 1 : 0), lu = w % ub;
-        const int r = pr * mb + 8 * lu;
-        if (r >= m) continue;
-        const uint4 v = __ldcg(reinterpret_cast<const uint4*>(p.p2p_win[par][self] + p.p2p_yarea) + r / 8);
-        store_half8(reinterpret_cast<uint8_t*>(p.y + r), v, m - r);
-      }
-    }
+    for (int kk = 0; kk < NS; ++kk) t[kk] = (ss0 + kk < p.sh.S) ? __ldcg(pp + (size_t)(ss0 + kk) * p.sh.m4) : 0.f;
+#pragma unroll
+    for (int kk = 0; kk < NS; ++kk)
+      if (ss0 + kk < p.sh.S) v += t[kk];
   }
-  // the last reducer to finish advances the round: every reducer has read it by now
-  __syncthreads();
-  if (threadIdx.x == 0 && atom_add_acq_rel_u32(cnt + 2, 1u) == nred - 1) {
-    cnt[2] = 0u;
-    *reinterpret_cast<volatile unsigned long long*>(p.p2p_sig[self] + 2) = round + 1ull;
+  return v;
+}
+
+// fp16 of this lane's row (low half) and of the next lane's row (high half): the LL payload
+__device__ __forceinline__ uint32_t half2_word(__half h) {
+  const uint32_t hb = (uint32_t)__half_as_ushort(h);
+  const uint32_t hn = __shfl_xor_sync(kFull, hb, 1);
+  return hb | (hn << 16);
+}
+
+// The round: every CTA's thread 0 reads it right after the PDL wait (the previous call is complete)
+// and counts in; the last CTA to count in -- every CTA has read it by then -- advances it at once
+// (the next call reads it after its own PDL wait).  Off the epilogue's path: no load or atomic
+// at the end of the kernel.
+__device__ __forceinline__ unsigned long long p2p_round_start(const KParams& p) {
+  const unsigned long long round = ld_acquire_u64(p.p2p_round);
+  unsigned* rcnt = p.counters + 2 * kFusedMaxJ + 2;
+  if (atom_add_acq_rel_u32(rcnt, 1u) == gridDim.x - 1) {
+    *rcnt = 0u;
+    *reinterpret_cast<volatile unsigned long long*>(const_cast<unsigned long long*>(p.p2p_round)) = round + 1ull;
+  }
+  return round;
+}
+
+template <int NS>
+__device__ __forceinline__ void p2p_epilogue(const KParams& p, unsigned long long round, int R, int ri, int g0,
+                                             int g1) {
+  const Shape& sh = p.sh;
+  const int P = p.npeers, self = p.p2p_self, tid = (int)threadIdx.x, lane = tid & 31;
+  const int par = (int)(round & 1ull);
+  const uint32_t stamp = (uint32_t)(round + 1ull);
+  uint8_t* const mine = p.p2p_win[par][self];
+  const int u0g = g0 / 2, u1g = (g1 + 1) / 2;  // the group's 8-row units (groups start on even quads)
+  const int r0 = 8 * (u0g + (int)((long long)(u1g - u0g) * ri / R));
+  const int r1 = min(sh.m, 8 * (u0g + (int)((long long)(u1g - u0g) * (ri + 1) / R)));
+  // warp-uniform loops (the half2 pairing shuffles): row r = base + lane, base even
+  if (p.p2p_mode == 1) {
+    const int ms = sh.m;  // ms % 8 == 0 (host-checked): row pairs never straddle a shard
+    for (int base = r0 + (tid & ~31); base < r1; base += kThreads) {
+      const int r = base + lane;
+      const bool ok = r < r1;
+      const __half h = __float2half_rn(ok ? row_sum<NS>(p, r) : 0.f);
+      if (ok) p.y[p.yoff + r] = h;
+      const uint32_t word = half2_word(h);
+      if (ok && !(lane & 1))
+        for (int pr = 0; pr < P; ++pr)
+          if (pr != self) st_ll(p.p2p_win[par][pr] + 4 * (size_t)(p.yoff + r), word, stamp);
+    }
+    for (int base = r0 + (tid & ~31); base < r1; base += kThreads) {
+      const int r = base + lane;
+      if (r < r1 && !(lane & 1))
+        for (int k = 0; k < P - 1; ++k) {
+          const int pr = k + (k >= self ? 1 : 0), rr = pr * ms + r;
+          const uint32_t w = ld_ll(mine + 4 * (size_t)rr, stamp);
+          p.y[rr] = __ushort_as_half((unsigned short)(w & 0xFFFFu));
+          p.y[rr + 1] = __ushort_as_half((unsigned short)(w >> 16));
+        }
+    }
+  } else {
+    const int m = sh.m, mb = p.p2p_mb, b0 = self * mb;
+    for (int base = r0 + (tid & ~31); base < r1; base += kThreads) {
+      const int r = base + lane;
+      if (r < r1) {
+        const float v = row_sum<NS>(p, r);
+        const int o = r / mb;
+        st_ll(p.p2p_win[par][o] + 8 * ((size_t)self * mb + (r - o * mb)), __float_as_uint(v), stamp);
+      }
+    }
+    // owned rows of this share: the P slots summed in rank order, fp16 -> y and every peer
+    const int lo = max(r0, b0), hi = min(r1, b0 + mb);  // multiples of 8 (or m)
+    for (int base = lo + (tid & ~31); base < hi; base += kThreads) {
+      const int r = base + lane;
+      const bool ok = r < hi;
+      float v = 0.f;
+      if (ok)
+        for (int pr = 0; pr < P; ++pr) v += __uint_as_float(ld_ll(mine + 8 * ((size_t)pr * mb + (r - b0)), stamp));
+      const __half h = __float2half_rn(v);
+      if (ok) p.y[r] = h;
+      if (P > 1) {
+        const uint32_t word = half2_word(h);
+        if (ok && !(lane & 1))
+          for (int pr = 0; pr < P; ++pr)
+            if (pr != self) st_ll(p.p2p_win[par][pr] + p.p2p_yarea + 4 * (size_t)r, word, stamp);
+      }
+    }
+    // the other owners' rows of this share, out of the local window
+    if (P > 1)
+      for (int base = r0 + (tid & ~31); base < r1; base += kThreads) {
+        const int r = base + lane;
+        if (r < r1 && !(lane & 1) && r / mb != self) {
+          const uint32_t w = ld_ll(mine + p.p2p_yarea + 4 * (size_t)r, stamp);
+          p.y[r] = __ushort_as_half((unsigned short)(w & 0xFFFFu));
+          if (r + 1 < m) p.y[r + 1] = __ushort_as_half((unsigned short)(w >> 16));
+        }
+      }
   }
 }
 
@@ -339,6 +302,8 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
         for (int d = 0; d < PD; ++d) load_quad(buf[d]);
       }
       pdl_wait();
+      if (EP && tid == 0)
+        *reinterpret_cast<unsigned long long*>(sm.misc_p + kMiscRound) = p2p_round_start(p);
       if (trace) trace[3] = globaltimer_ns();
       if (warp == 0 && !p.xdirect)
         stage_x(xbuf0, bar0, p.x, sh.n, s * kSliceCols, slice_cols(sh.n, s), 32, 1, 1, lane);
@@ -463,7 +428,9 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
       if (sh.S <= 16) reduce_rows(std::integral_constant<int, 16>{});
       else reduce_rows(std::integral_constant<int, 48>{});
     } else {
-      p2p_epilogue(p, J, R, fj, ri, g0, g1);
+      const unsigned long long round = *reinterpret_cast<const unsigned long long*>(sm.misc_p + kMiscRound);
+      if (sh.S <= 16) p2p_epilogue<16>(p, round, R, ri, g0, g1);
+      else p2p_epilogue<48>(p, round, R, ri, g0, g1);
     }
     if (trace) trace[6] = globaltimer_ns();  // reduction share done
     return;

@@ -55,6 +55,7 @@ std::atomic<unsigned long long> g_launches{0};
 
 // arrival counters and epochs of the fused reduction, then the grid-wide
 // done counter of the fused rows all-gather (256-byte aligned)
+// [2][kFusedMaxJ] arrival / departure counters, 64 misc words (the P2P round-advance counter at word 2)
 static size_t counters_bytes(const Shape&) { return 2u * kFusedMaxJ * 4u + 256u; }
 
 int batch_pad(int b) {
@@ -128,7 +129,6 @@ static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint1
     const bool on = pa && i < pa->npeers;
     p.p2p_win[0][i] = on ? pa->win[0][i] : nullptr;
     p.p2p_win[1][i] = on ? pa->win[1][i] : nullptr;
-    p.p2p_sig[i] = on ? pa->sig[i] : nullptr;
   }
   p.data = static_cast<const uint8_t*>(data);
   p.x = reinterpret_cast<const __half*>(x);

@@ -55,13 +55,13 @@ struct KParams {
   int xdirect;       // GEMV: each thread loads its 8 x values for the LUT build straight from global memory
                      // (0: the slice is staged into shared memory by the bulk-copy engine first)
   int reducers;      // GEMV fused mode: the last R CTAs to arrive in a row-quad group reduce it
-  // fused tensor-parallel epilogue over peer memory (NEXT-1, lutgemm_p2p.cu).  p2p_mode 1 (rows
-  // all-gather): each finished fp16 row r goes to window[par][pr] + p2p_yarea + 2 (yoff + r) of every
-  // rank pr; p2p_mode 2 (column split, reduce-scatter): each fp32 partial row r goes to its owner
-  // o = r / p2p_mb, slot [p2p_self][r - o p2p_mb] of window[par][o].  par = *p2p_round & 1 (device-side
-  // round counter: graph-capturable).  The grid's last reducer then signals every rank (p2p_sig[pr]).
+  // fused tensor-parallel epilogue over peer memory (NEXT-1, lutgemm_p2p.cu, gemv_kernel.cuh
+  // p2p_epilogue): LL words (data | stamp << 32) into the ranks' windows.  p2p_mode 1 (rows
+  // all-gather): rows (r, r+1) of the gathered output at window[par][pr] + 4 (yoff + r);
+  // p2p_mode 2 (column split): the fp32 row r at its owner o = r / p2p_mb, slot [self][r - o mb]
+  // (8-byte words), the owner's fp16 rows (r, r+1) at p2p_yarea + 4 r.  par = *p2p_round & 1
+  // (device-side round: graph-capturable), stamp = low 32 bits of *p2p_round + 1.
   uint8_t* p2p_win[2][8];
-  unsigned long long* p2p_sig[8];
   const unsigned long long* p2p_round;
   int p2p_mode;      // 0: plain output
   int npeers;
@@ -96,7 +96,6 @@ cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, in
 // GEMV mode (returns cudaErrorNotSupported otherwise).
 struct P2PArgs {
   uint8_t* win[2][8];
-  unsigned long long* sig[8];
   const unsigned long long* round;
   int mode, npeers, self, yoff, mb;
   unsigned yarea;

@@ -2,27 +2,32 @@
 // over peer memory (the paper names GPU-to-GPU communication as what limits
 // tensor parallelism once the matmul is fast, Table 2).
 //
-// Every rank owns two exchange windows (double buffer) and a 256-byte signal block, allocated
-// with cudaMalloc and shared through CUDA IPC handles that the caller exchanges (any transport;
-// the Python binding uses torch.distributed).  A call is
-// one kernel launch, graph-capturable (no host-side state changes between calls: the round number
-// lives on the device).
+// Every rank owns two exchange windows (double buffer, selected by the parity of a device-side
+// round counter) allocated with cudaMalloc and shared through CUDA IPC handles that the caller
+// exchanges (any transport; the Python binding uses torch.distributed).  A call is one kernel
+// launch, graph-capturable (no host-side state changes between calls).
 //
-// The whole exchange runs in the fused GEMV's epilogue (lutgemm_gemv.cu, p2p_epilogue), in the
-// reducer CTAs (all resident), 16-byte stores over NVLink / NVSwitch P2P mappings:
-//   rows (m-split, ROWS_ALLGATHER): fp16 rows of this rank's shard -> this rank's y and every
-//     peer's window; signal; wait for the round's P signals; copy the peers' rows window -> y;
-//   cols (n-split, COLS_ALLREDUCE): reduce-scatter + all-gather: fp32 partial rows -> the row's
-//     OWNER rank only (rank o owns rows [o mb, (o+1) mb)), slot [this rank]; signal; wait; the
-//     owner sums its block over the P slots in rank order (deterministic, identical on every
-//     rank), rounds to fp16 and stores it into y and every peer's window; signal; wait; copy the
-//     peers' blocks window -> y.
-// The last reducer advances the device-side round (the parity of the double buffer).
+// The whole exchange runs in the fused GEMV's epilogue (gemv_kernel.cuh, p2p_epilogue), in the
+// reducer CTAs, one thread per output row, as LL words over the NVLink / NVSwitch P2P mappings:
+// 8-byte stores of 4 data bytes + a 4-byte round stamp, read back by polling the stamp (NCCL's
+// LL protocol for small messages: no fence, no separate signal, no barrier).  Every rank runs
+// the same reducer partition, so reducer (group, share) waits only for the same share's words
+// of the other ranks:
+//   rows (m-split, ROWS_ALLGATHER): fp16 row pairs of this rank's shard -> y and every peer's
+//     window; the peers' rows of the same share out of the local window -> y;
+//   cols (n-split, COLS_ALLREDUCE): reduce-scatter + all-gather: fp32 rows -> the row's OWNER
+//     rank only (rank o owns rows [o mb, (o+1) mb)), slot [this rank]; the owner sums its rows
+//     over the P slots in rank order (deterministic, identical on every rank), rounds to fp16 and
+//     sends the row pairs to every peer; the other owners' rows out of the local window -> y.
+// The last reducer advances the round.
 //
 // Flow control: window (k & 1) is rewritten in round k + 2 only; a rank enters round k + 2 after
-// completing round k + 1, which needs every peer's round-(k+1) signal, sent after that peer's
-// stream completed its round-k GEMV (round k + 1's epilogue starts after its PDL wait).
-// Signal counters are 64-bit (no wrap).  Every rank makes the same sequence of calls.
+// completing round k + 1, in which it received at least one round-(k+1) word from every peer
+// (rows: every share reads every peer; columns: every rank owns rows, host-checked, and the
+// owner reads every peer's slot), each written after that peer's stream completed its round-k
+// call (round k + 1's epilogue starts after its PDL wait).  A stale word of the same parity
+// carries stamp - 2; stamps are 32 bits, so a word would have to sit unwritten for a multiple
+// of 2^32 rounds to be mistaken.  Every rank makes the same sequence of calls.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -37,9 +42,9 @@ lutgemm_status lutgemm_internal_fail(lutgemm_status st, const char* msg);
 lutgemm_status lutgemm_internal_check_weight(const lutgemm_weight* w);
 lutgemm_status lutgemm_internal_check_device();
 
-// signal block (256 bytes, device): [0] signal A (epilogue stores done), [1] signal B (cols:
-// all-gather stores done), [2] round (local)
-constexpr int kSigA = 0, kRound = 2;
+// signal block (device, 256 bytes): word 0 = the round (local; the LL words carry the signals)
+constexpr int kRound = 0;
+constexpr size_t kSigBytes = 256;
 
 struct lutgemm_p2p {
   int rank, nranks, dev;
@@ -79,6 +84,8 @@ lutgemm_status run(lutgemm_p2p* g, int mode, const lutgemm_weight* shard, const 
     return lutgemm_internal_fail(LUTGEMM_ERR_INVALID_ARG, "rows all-gather needs m_shard % 8 == 0");
   const int m_out = mode == 1 ? P * ms : ms;
   const int mb = block_rows(ms, P);
+  if (mode == 2 && (long long)(P - 1) * mb >= ms)  // flow control needs a flag from every peer per call
+    return lutgemm_internal_fail(LUTGEMM_ERR_INVALID_ARG, "column all-reduce: every rank must own rows (m too small for P)");
   const size_t need = lutgemm_p2p_window_bytes(P, mode == 1 ? LUTGEMM_TP_ROWS_ALLGATHER : LUTGEMM_TP_COLS_ALLREDUCE,
                                                m_out);
   if (need > g->win_bytes)
@@ -97,7 +104,6 @@ lutgemm_status run(lutgemm_p2p* g, int mode, const lutgemm_weight* shard, const 
   for (int pr = 0; pr < 8; ++pr) {
     a.win[0][pr] = pr < P ? g->peer_win[0][pr] : nullptr;
     a.win[1][pr] = pr < P ? g->peer_win[1][pr] : nullptr;
-    a.sig[pr] = pr < P ? g->peer_sig[pr] + kSigA : nullptr;
   }
   a.round = g->sig + kRound;
   a.mode = mode;
@@ -105,7 +111,7 @@ lutgemm_status run(lutgemm_p2p* g, int mode, const lutgemm_weight* shard, const 
   a.self = g->rank;
   a.yoff = mode == 1 ? g->rank * ms : 0;
   a.mb = mb;
-  a.yarea = mode == 1 ? 0u : (unsigned)align256((size_t)P * mb * 4);
+  a.yarea = mode == 1 ? 0u : (unsigned)align256((size_t)P * mb * 8);
   cudaError_t e = lg::run_gemv_p2p(sh, shard->data, x, ws, a, y, s);
   if (e == cudaErrorNotSupported)
     return lutgemm_internal_fail(LUTGEMM_ERR_UNSUPPORTED, "shard shape does not run the fused GEMV mode");
@@ -118,10 +124,11 @@ extern "C" {
 
 size_t lutgemm_p2p_window_bytes(int nranks, int mode, int m) {
   if (nranks < 1 || nranks > 8 || m < 1) return 0;
-  if (mode == LUTGEMM_TP_ROWS_ALLGATHER) return align256((size_t)m * 2);
+  // LL words (8 bytes: 4 data + 4 stamp): rows = half2 per word; cols = fp32 slots, then half2 rows
+  if (mode == LUTGEMM_TP_ROWS_ALLGATHER) return align256((size_t)m * 4);
   if (mode == LUTGEMM_TP_COLS_ALLREDUCE) {
     const size_t mb = (size_t)block_rows(m, nranks);
-    return align256((size_t)nranks * mb * 4) + align256((size_t)nranks * mb * 2);
+    return align256((size_t)nranks * mb * 8) + align256((size_t)nranks * mb * 4);
   }
   return 0;
 }
@@ -139,8 +146,8 @@ lutgemm_status lutgemm_p2p_create(int rank, int nranks, size_t win_bytes, lutgem
   cudaGetDevice(&g->dev);
   cudaError_t e = cudaMalloc(&g->win[0], g->win_bytes);
   if (e == cudaSuccess) e = cudaMalloc(&g->win[1], g->win_bytes);
-  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&g->sig), 256);
-  if (e == cudaSuccess) e = cudaMemset(g->sig, 0, 256);
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&g->sig), kSigBytes);
+  if (e == cudaSuccess) e = cudaMemset(g->sig, 0, kSigBytes);
   if (e == cudaSuccess) e = cudaMemset(g->win[0], 0, g->win_bytes);
   if (e == cudaSuccess) e = cudaMemset(g->win[1], 0, g->win_bytes);
   memset(record, 0, kRec);

@@ -144,8 +144,15 @@ class PackedBCQ:
     fmt: int = FMT_BCQ
 
     @classmethod
-    def empty(cls, m, n, q, g, has_offset, device, fmt: int = FMT_BCQ) -> "PackedBCQ":
-        data = torch.empty(lutgemm_packed_bytes(m, n, q, g, has_offset, fmt), dtype=torch.uint8, device=device)
+    def empty(cls, m, n, q, g, has_offset, device, fmt: int = FMT_BCQ, out: torch.Tensor | None = None) -> "PackedBCQ":
+        nb = lutgemm_packed_bytes(m, n, q, g, has_offset, fmt)
+        if out is None:
+            data = torch.empty(nb, dtype=torch.uint8, device=device)
+        else:  # caller-provided storage (e.g. a view into one arena holding many layers)
+            if out.dtype != torch.uint8 or not out.is_cuda or not out.is_contiguous() or out.numel() < nb \
+                    or out.data_ptr() % 256:
+                raise ValueError(f"out must be a contiguous 256-byte aligned CUDA uint8 tensor of >= {nb} bytes")
+            data = out[:nb]
         w = cls(m, n, q, g, has_offset, data, fmt=fmt)
         w.struct = lutgemm_weight(m, n, q, g, int(has_offset), int(fmt), data.data_ptr())
         return w
@@ -155,14 +162,14 @@ class PackedBCQ:
 
 
 def lutgemm_pack_bcq(planes: torch.Tensor, alpha: torch.Tensor, offset: torch.Tensor | None, n: int, g: int,
-                     stream=None) -> PackedBCQ:
+                     stream=None, out: torch.Tensor | None = None) -> PackedBCQ:
     """Canonical BCQ (device tensors: planes int32/uint32 [q][m][n/32], alpha fp16
-    [m][n/g][q], offset fp16 [m][n/g] or None) -> PackedBCQ."""
+    [m][n/g][q], offset fp16 [m][n/g] or None) -> PackedBCQ (in `out`, a uint8 device view, if given)."""
     q, m = int(planes.shape[0]), int(planes.shape[1])
     for t in (planes, alpha, offset):
         if t is not None and (not t.is_cuda or not t.is_contiguous()):
             raise ValueError("pack sources must be contiguous CUDA tensors")
-    w = PackedBCQ.empty(m, n, q, g, offset is not None, planes.device)
+    w = PackedBCQ.empty(m, n, q, g, offset is not None, planes.device, out=out)
     src = lutgemm_pack_src(SRC_BCQ, m, n, q, g, 0, planes.data_ptr(), alpha.data_ptr(), _ptr(offset), None, None,
                            None)
     _check("lutgemm_pack_bcq", lib.lutgemm_pack_bcq(ctypes.byref(src), ctypes.byref(w.struct), _stream(stream)))

@@ -145,7 +145,8 @@ def test_p2p_argument_validation_without_gpu():
             st = fn(None, ctypes.byref(w), 4096, 8192, 1 << 20, None, 16384)
             assert st in (1, 2) and msg in lib.lutgemm_last_error(), (bad, lib.lutgemm_last_error())
     # window sizes: rows = 2 m (256-B rounded); cols = P mb fp32 slots + P mb fp16, mb = 8 ceil(ceil(m/P)/8)
-    assert lib.lutgemm_p2p_window_bytes(8, B.TP_ROWS_ALLGATHER, 49152) == 98304
-    assert lib.lutgemm_p2p_window_bytes(8, B.TP_COLS_ALLREDUCE, 12288) == 8 * 1536 * 4 + 8 * 1536 * 2
-    assert lib.lutgemm_p2p_window_bytes(3, B.TP_COLS_ALLREDUCE, 100) == 512 + 256  # mb = 40: 480 B + 240 B, 256-B rounded
+    # LL words: 8 bytes per half2 row pair (rows), per fp32 slot row and per half2 row pair (cols)
+    assert lib.lutgemm_p2p_window_bytes(8, B.TP_ROWS_ALLGATHER, 49152) == 49152 * 4
+    assert lib.lutgemm_p2p_window_bytes(8, B.TP_COLS_ALLREDUCE, 12288) == 8 * 1536 * 8 + 8 * 1536 * 4
+    assert lib.lutgemm_p2p_window_bytes(3, B.TP_COLS_ALLREDUCE, 100) == 1024 + 512  # mb = 40: 960 B + 480 B, 256-B rounded
     assert lib.lutgemm_p2p_window_bytes(9, B.TP_COLS_ALLREDUCE, 100) == 0

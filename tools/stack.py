@@ -62,6 +62,10 @@ def main():
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--tp-impl", default="nccl", choices=["nccl", "p2p"])
     ap.add_argument("--same-device", action="store_true")
+    ap.add_argument("--arena", action="store_true",
+                    help="all packed weights in one device allocation (2 MB aligned views)")
+    ap.add_argument("--graph-layers", type=int, default=0,
+                    help="layers per CUDA graph (default: the whole token in one graph)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -81,6 +85,14 @@ def main():
         p2p = L.P2PGroup(rank, world, cols_m=H)
 
     t0 = time.time()
+    arena, aoff = None, 0
+    if args.arena:
+        A2 = 2 << 20
+        sizes = [(L.lutgemm_packed_bytes(m // world, n, Q, G, False) if s == "rows" else
+                  L.lutgemm_packed_bytes(m, n // world, Q, G, False)) for _, m, n, s in LINEARS]
+        arena = torch.empty(args.layers * sum((z + A2 - 1) // A2 * A2 for z in sizes) + A2, dtype=torch.uint8,
+                            device=dev)
+        aoff = (-arena.data_ptr()) % A2
     weights = []  # per layer: dict name -> PackedBCQ
     check_rows = {}
     rng = np.random.default_rng(0)
@@ -95,7 +107,12 @@ def main():
                 idx = torch.from_numpy(rows).to(dev)
                 check_rows[(layer, name)] = (rows, planes[:, idx].cpu().numpy().view(np.uint32),
                                              alpha[idx].cpu().numpy(), ms, ns)
-            lw[name] = L.lutgemm_pack_bcq(planes, alpha, None, ns, G)
+            out = None
+            if arena is not None:
+                nb = L.lutgemm_packed_bytes(ms, ns, Q, G, False)
+                out = arena[aoff:aoff + nb]
+                aoff += (nb + (2 << 20) - 1) // (2 << 20) * (2 << 20)
+            lw[name] = L.lutgemm_pack_bcq(planes, alpha, None, ns, G, out=out)
             del planes, alpha
         weights.append(lw)
     torch.cuda.synchronize()
@@ -126,9 +143,10 @@ def main():
         else:
             comm.linear(L.TP_COLS_ALLREDUCE, w, xin, y, tws)
 
-    def token():
-        x.copy_(x0)  # every token starts from the same input (device-to-device copy)
-        for lw in weights:
+    def token(l0=0, l1=None):
+        if l0 == 0:
+            x.copy_(x0)  # every token starts from the same input (device-to-device copy)
+        for lw in weights[l0:l1]:
             L.lutgemm_gemv(lw["qkv"], x, qkv_o, ws)
             cols(lw["out"], qkv_o[:H // world], out_o)
             L.lutgemm_gemv(lw["fc1"], out_o, fc1_o, ws)
@@ -136,11 +154,21 @@ def main():
 
     token()
     torch.cuda.synchronize()
-    graph = torch.cuda.CUDAGraph()
+    gl = args.graph_layers if args.graph_layers > 0 else args.layers
+    graphs = []
     cap = torch.cuda.Stream()
     cap.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.graph(graph, stream=cap):
-        token()
+    for l0 in range(0, args.layers, gl):
+        graphs.append(torch.cuda.CUDAGraph())
+        with torch.cuda.graph(graphs[-1], stream=cap):
+            token(l0, l0 + gl)
+
+    class _Token:  # one token = the graphs in order
+        @staticmethod
+        def replay():
+            for gr in graphs:
+                gr.replay()
+    graph = _Token
     for _ in range(args.warmup):
         graph.replay()
     torch.cuda.synchronize()
@@ -209,7 +237,7 @@ def main():
     if rank == 0:
         print(json.dumps({
             "config": "OPT-175B decoder linear stack (96 x QKV/out/fc1/fc2), q=3 g=128, b=1",
-            "layers": args.layers, "tp": world, "tp_impl": args.tp_impl if world > 1 or p2p else None,
+            "layers": args.layers, "graph_layers": gl, "arena": args.arena, "tp": world, "tp_impl": args.tp_impl if world > 1 or p2p else None,
             "x_sha": x_sha,
             "ms_per_token": round(ms, 4),
             "GBps_per_gpu": round(bytes_token / (ms * 1e-3) / 1e9, 1),
