@@ -102,20 +102,11 @@ __device__ __forceinline__ uint32_t half2_word(__half h) {
   return hb | (hn << 16);
 }
 
-// The round: every CTA's thread 0 reads it right after the PDL wait (the previous call is complete)
-// and counts in; the last CTA to count in -- every CTA has read it by then -- advances it at once
-// (the next call reads it after its own PDL wait).  Off the epilogue's path: no load or atomic
-// at the end of the kernel.
-__device__ __forceinline__ unsigned long long p2p_round_start(const KParams& p) {
-  const unsigned long long round = ld_acquire_u64(p.p2p_round);
-  unsigned* rcnt = p.counters + 2 * kFusedMaxJ + 2;
-  if (atom_add_acq_rel_u32(rcnt, 1u) == gridDim.x - 1) {
-    *rcnt = 0u;
-    *reinterpret_cast<volatile unsigned long long*>(const_cast<unsigned long long*>(p.p2p_round)) = round + 1ull;
-  }
-  return round;
-}
-
+// The round: every CTA's thread 0 reads it right after the PDL wait (the previous call is complete:
+// a relaxed load suffices) and counts in with a release RMW -- neither result is waited for until
+// the main loop is over, so nothing stalls the LUT build.  After its main loop the CTA that counted
+// in last (every CTA had read the round before counting in) acquires and advances it; the next
+// call reads it after its own PDL wait.  The reducers take the round from shared memory.
 template <int NS>
 __device__ __forceinline__ void p2p_epilogue(const KParams& p, unsigned long long round, int R, int ri, int g0,
                                              int g1) {
@@ -151,28 +142,27 @@ __device__ __forceinline__ void p2p_epilogue(const KParams& p, unsigned long lon
         }
     }
   } else {
-    const int m = sh.m, mb = p.p2p_mb, b0 = self * mb;
+    const int m = sh.m, mb = p.p2p_mb;
+    // each fp32 row to its owner's slot [self]; on the owner the same thread sums its owned rows
+    // over the P slots in rank order (its own slot's value straight from the register), rounds to
+    // fp16 and sends the row pairs to every peer.  Every rank sends an iteration's rows before it
+    // waits for that iteration's words, so the waits cannot deadlock.
     for (int base = r0 + (tid & ~31); base < r1; base += kThreads) {
       const int r = base + lane;
-      if (r < r1) {
-        const float v = row_sum<NS>(p, r);
-        const int o = r / mb;
-        st_ll(p.p2p_win[par][o] + 8 * ((size_t)self * mb + (r - o * mb)), __float_as_uint(v), stamp);
-      }
-    }
-    // owned rows of this share: the P slots summed in rank order, fp16 -> y and every peer
-    const int lo = max(r0, b0), hi = min(r1, b0 + mb);  // multiples of 8 (or m)
-    for (int base = lo + (tid & ~31); base < hi; base += kThreads) {
-      const int r = base + lane;
-      const bool ok = r < hi;
-      float v = 0.f;
-      if (ok)
-        for (int pr = 0; pr < P; ++pr) v += __uint_as_float(ld_ll(mine + 8 * ((size_t)pr * mb + (r - b0)), stamp));
-      const __half h = __float2half_rn(v);
-      if (ok) p.y[r] = h;
+      const bool ok = r < r1;
+      const float v = ok ? row_sum<NS>(p, r) : 0.f;
+      const int o = r / mb;
+      const bool own = ok && o == self;
+      if (ok && !own) st_ll(p.p2p_win[par][o] + 8 * ((size_t)self * mb + (r - o * mb)), __float_as_uint(v), stamp);
+      float sum = 0.f;
+      if (own)
+        for (int pr = 0; pr < P; ++pr)
+          sum += pr == self ? v : __uint_as_float(ld_ll(mine + 8 * ((size_t)pr * mb + (r - o * mb)), stamp));
+      const __half h = __float2half_rn(sum);
+      if (own) p.y[r] = h;
       if (P > 1) {
         const uint32_t word = half2_word(h);
-        if (ok && !(lane & 1))
+        if (own && !(lane & 1))
           for (int pr = 0; pr < P; ++pr)
             if (pr != self) st_ll(p.p2p_win[par][pr] + p.p2p_yarea + 4 * (size_t)r, word, stamp);
       }
@@ -238,6 +228,8 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     __syncthreads();
   }
 
+  unsigned long long p2p_rd = 0;  // EP: the round (thread 0) and its count-in rank
+  unsigned p2p_k = 0;
   constexpr int NB = PD + 1;  // ring of quad buffers: the load of quad t + PD is issued before quad t is computed
   int e = 0;
   long long it = it0;
@@ -247,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     if (J > 0) {
       s = fs;
       rq_a = p.gq[fj];
-      rq_b = p.gq[fj + 1];
+      rq_b = p.gq[fj + 1] - p.pool_t;  // the group's last pool_t quads go to the slice's pool
     } else {
       s = (int)(it / sh.RQ);
       rq_a = (int)(it - (long long)s * sh.RQ);
@@ -302,8 +294,10 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
         for (int d = 0; d < PD; ++d) load_quad(buf[d]);
       }
       pdl_wait();
-      if (EP && tid == 0)
-        *reinterpret_cast<unsigned long long*>(sm.misc_p + kMiscRound) = p2p_round_start(p);
+      if (EP && tid == 0) {
+        p2p_rd = ld_relaxed_u64(p.p2p_round);
+        p2p_k = atom_add_release_u32(p.counters + 2 * kFusedMaxJ + 2, 1u);
+      }
       if (trace) trace[3] = globaltimer_ns();
       if (warp == 0 && !p.xdirect)
         stage_x(xbuf0, bar0, p.x, sh.n, s * kSliceCols, slice_cols(sh.n, s), 32, 1, 1, lane);
@@ -368,6 +362,57 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
 #pragma unroll
     for (int d = 0; d < NB - 1; ++d)
       if (t0 + d < nt) quad(buf[d]);
+    if (J > 0 && p.pool_t > 0) {
+      // Tail pool: the last T quads of every group of slice s, claimed one at a time by whichever
+      // warp of the slice's J CTAs is free (two claims in flight: the next claim and the quad's
+      // loads overlap the current quad).  Same LUT, same partial slots: the result is bitwise the
+      // same whoever computes a quad.  Each finished quad counts in on the slice's `done` word.
+      unsigned* pc = p.counters + kPoolCounters + 3 * s;
+      const int T = p.pool_t, NPQ = J * T;
+      auto claim = [&]() {
+        int c = 0;
+        if (lane == 0) c = (int)atomicAdd(pc, 1u);
+        return __shfl_sync(kFull, c, 0);
+      };
+      auto load_at = [&](Ring<QT>& b, int c) {
+        const int j = c / T, rq = p.gq[j + 1] - T + (c - j * T);
+        const uint8_t* kq = la.kp + (size_t)rq * la.KB;
+        const uint8_t* aq = la.ap + (size_t)rq * la.AB;
+        const uint8_t* zq = la.zp + (size_t)rq * la.ZB;
+#pragma unroll
+        for (int i = 0; i < QT; ++i)
+          if (QT <= 4 || i < q) b.k[i] = ldg_stream_u4(kq + i * la.kstride);
+        if (QT == 8) {
+          b.ap = aq;
+          b.zp = zq;
+        }
+        if (!cg) {
+#pragma unroll
+          for (int i = 0; i < QT; ++i)
+            if ((QT <= 4 || i < q) && (!CMP || i == 0)) b.a[i] = ldg_nc_u2(aq + 8 * i);
+          if (HAS_Z) b.z = ldg_nc_u2(zq);
+        }
+        return rq;
+      };
+      int c = claim();
+      int rq = c < NPQ ? load_at(buf[0], c) : 0;
+      int cn = claim();
+      while (c < NPQ) {
+        const int rqn = cn < NPQ ? load_at(buf[1], cn) : 0;
+        const int cnn = cn < NPQ ? claim() : cn;
+        pw = p.partial + (size_t)s * sh.m4 + 4 * rq + (lane >> 3);
+        quad(buf[0]);
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          atomicAdd(pc + 1, 1u);
+        }
+        buf[0] = buf[1];
+        rq = rqn;
+        c = cn;
+        cn = cnn;
+      }
+    }
     __syncthreads();  // the LUT and x buffer are reused by the next segment
     if (trace) trace[e == 0 ? 4 : 6] = globaltimer_ns();  // all warps done
     it = itn;
@@ -386,11 +431,32 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     // departure atomic on the way out).  Release: the CTA's partial stores (ordered before by the
     // barrier) are visible to whoever acquires the count.
     unsigned* arrive = p.counters + fj;
+    if (EP && tid == 0) {
+      *reinterpret_cast<unsigned long long*>(sm.misc_p + kMiscRound) = p2p_rd;
+      if (p2p_k == gridDim.x - 1) {  // the last to count in: every CTA has read the round
+        unsigned* rcnt = p.counters + 2 * kFusedMaxJ + 2;
+        fence_acq_rel_gpu();
+        *rcnt = 0u;
+        *reinterpret_cast<volatile unsigned long long*>(const_cast<unsigned long long*>(p.p2p_round)) = p2p_rd + 1ull;
+      }
+    }
     __syncthreads();  // all partial stores of this CTA are issued
     if (tid == 0) {
       // wrapping arrival counter: k = arrivals before this one; it returns to 0 with the S-th, so a
       // reducer that is not last waits until the counter falls to <= k (acquire: synchronizes with
       // the last arriver's RMW, which acquired every earlier arrival's partial stores)
+      if (p.pool_t > 0) {
+        // the slice's pool is complete (the other CTAs' last quads included) before this CTA
+        // counts in; the last of the J CTAs to see it resets the slice's pool counters
+        unsigned* pc = p.counters + kPoolCounters + 3 * fs;
+        const unsigned npq = (unsigned)(J * p.pool_t);
+        while (ld_acquire_u32(pc + 1) < npq) __nanosleep(32);
+        if (atom_add_acq_rel_u32(pc + 2, 1u) == (unsigned)J - 1u) {
+          pc[0] = 0u;
+          pc[1] = 0u;
+          pc[2] = 0u;
+        }
+      }
       const unsigned kk = atom_inc_acq_rel_u32(arrive, (unsigned)sh.S - 1u);
       if (kk >= (unsigned)(sh.S - R) && kk != (unsigned)sh.S - 1u)
         while (ld_acquire_u32(arrive) > kk) __nanosleep(32);

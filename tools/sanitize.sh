@@ -1,4 +1,6 @@
 #!/bin/bash
+# NOTE: the GPU pool this repo is measured on has disabled compute-sanitizer (its wrapper exits 86);
+# tests/test_gpu_sanitize.py skips there.  Round-1 results: profiles/r01_sanitizers.md.
 # compute-sanitizer over every kernel path (tier T4); summaries to gpurun_out/sanitize_*.txt
 set -u
 mkdir -p gpurun_out
