@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
     if (J > 0) {
       s = fs;
       rq_a = p.gq[fj];
-      rq_b = p.gq[fj + 1] - p.pool_t;  // the group's last pool_t quads go to the slice's pool
+      rq_b = p.gq[fj + 1];
     } else {
       s = (int)(it / sh.RQ);
       rq_a = (int)(it - (long long)s * sh.RQ);
@@ -362,57 +362,6 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
 #pragma unroll
     for (int d = 0; d < NB - 1; ++d)
       if (t0 + d < nt) quad(buf[d]);
-    if (J > 0 && p.pool_t > 0) {
-      // Tail pool: the last T quads of every group of slice s, claimed one at a time by whichever
-      // warp of the slice's J CTAs is free (two claims in flight: the next claim and the quad's
-      // loads overlap the current quad).  Same LUT, same partial slots: the result is bitwise the
-      // same whoever computes a quad.  Each finished quad counts in on the slice's `done` word.
-      unsigned* pc = p.counters + kPoolCounters + 3 * s;
-      const int T = p.pool_t, NPQ = J * T;
-      auto claim = [&]() {
-        int c = 0;
-        if (lane == 0) c = (int)atomicAdd(pc, 1u);
-        return __shfl_sync(kFull, c, 0);
-      };
-      auto load_at = [&](Ring<QT>& b, int c) {
-        const int j = c / T, rq = p.gq[j + 1] - T + (c - j * T);
-        const uint8_t* kq = la.kp + (size_t)rq * la.KB;
-        const uint8_t* aq = la.ap + (size_t)rq * la.AB;
-        const uint8_t* zq = la.zp + (size_t)rq * la.ZB;
-#pragma unroll
-        for (int i = 0; i < QT; ++i)
-          if (QT <= 4 || i < q) b.k[i] = ldg_stream_u4(kq + i * la.kstride);
-        if (QT == 8) {
-          b.ap = aq;
-          b.zp = zq;
-        }
-        if (!cg) {
-#pragma unroll
-          for (int i = 0; i < QT; ++i)
-            if ((QT <= 4 || i < q) && (!CMP || i == 0)) b.a[i] = ldg_nc_u2(aq + 8 * i);
-          if (HAS_Z) b.z = ldg_nc_u2(zq);
-        }
-        return rq;
-      };
-      int c = claim();
-      int rq = c < NPQ ? load_at(buf[0], c) : 0;
-      int cn = claim();
-      while (c < NPQ) {
-        const int rqn = cn < NPQ ? load_at(buf[1], cn) : 0;
-        const int cnn = cn < NPQ ? claim() : cn;
-        pw = p.partial + (size_t)s * sh.m4 + 4 * rq + (lane >> 3);
-        quad(buf[0]);
-        __syncwarp();
-        if (lane == 0) {
-          __threadfence();
-          atomicAdd(pc + 1, 1u);
-        }
-        buf[0] = buf[1];
-        rq = rqn;
-        c = cn;
-        cn = cnn;
-      }
-    }
     __syncthreads();  // the LUT and x buffer are reused by the next segment
     if (trace) trace[e == 0 ? 4 : 6] = globaltimer_ns();  // all warps done
     it = itn;
@@ -445,18 +394,6 @@ __global__ void __launch_bounds__(kThreads, 1) lut_gemv_kernel(const KParams p) 
       // wrapping arrival counter: k = arrivals before this one; it returns to 0 with the S-th, so a
       // reducer that is not last waits until the counter falls to <= k (acquire: synchronizes with
       // the last arriver's RMW, which acquired every earlier arrival's partial stores)
-      if (p.pool_t > 0) {
-        // the slice's pool is complete (the other CTAs' last quads included) before this CTA
-        // counts in; the last of the J CTAs to see it resets the slice's pool counters
-        unsigned* pc = p.counters + kPoolCounters + 3 * fs;
-        const unsigned npq = (unsigned)(J * p.pool_t);
-        while (ld_acquire_u32(pc + 1) < npq) __nanosleep(32);
-        if (atom_add_acq_rel_u32(pc + 2, 1u) == (unsigned)J - 1u) {
-          pc[0] = 0u;
-          pc[1] = 0u;
-          pc[2] = 0u;
-        }
-      }
       const unsigned kk = atom_inc_acq_rel_u32(arrive, (unsigned)sh.S - 1u);
       if (kk >= (unsigned)(sh.S - R) && kk != (unsigned)sh.S - 1u)
         while (ld_acquire_u32(arrive) > kk) __nanosleep(32);

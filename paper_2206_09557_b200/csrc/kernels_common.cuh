@@ -25,9 +25,6 @@ constexpr int kMiscBytes = 8192;       // x double buffer (2 x 2 KB) + mbarriers
 // everywhere (measured and dropped): the larger carveout takes L1 capacity.
 constexpr int kSmemBytesBase = 3 * 65536;
 constexpr int kMiscArrive = 4128;      // misc-block offset of the fused reduction's arrival slot (u32)
-// workspace counter words: [2][kFusedMaxJ] arrival / departure, 64 misc (P2P round count at
-// word 2), then [kFusedMaxJ][3] per-slice tail-pool counters (claim, done, leave)
-constexpr int kPoolCounters = 2 * kFusedMaxJ + 64;
 constexpr int kMiscRound = 4136;       // misc-block offset of the P2P round read at kernel start (u64)
 constexpr unsigned kFull = 0xffffffffu;
 

@@ -55,8 +55,8 @@ std::atomic<unsigned long long> g_launches{0};
 
 // arrival counters and epochs of the fused reduction, then the grid-wide
 // done counter of the fused rows all-gather (256-byte aligned)
-// counter words (kernels_common.cuh): arrival / departure, misc, per-slice tail-pool counters
-static size_t counters_bytes(const Shape&) { return (size_t)(kPoolCounters + 3 * kFusedMaxJ) * 4u; }
+// [2][kFusedMaxJ] arrival / departure counters, 64 misc words (the P2P round-advance counter at word 2)
+static size_t counters_bytes(const Shape&) { return 2u * kFusedMaxJ * 4u + 256u; }
 
 int batch_pad(int b) {
   int bp = 1;
@@ -205,12 +205,6 @@ static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint1
       p.reducers = (int)std::min<long long>(sh.S, (red_bytes + 8191) / 8192);  // ~8 KB of partials per reducer
       const char* env = getenv("LUTGEMM_GEMV_REDUCERS");
       if (env && atoi(env) > 0) p.reducers = std::min(atoi(env), sh.S);
-      // tail pool: T quads of every group (a few per warp; the per-SM main-loop speed differs by
-      // +-2.5 %, consistently, so a static split leaves the fast CTAs of a slice idle at the end)
-      static const int pool_env = getenv("LUTGEMM_POOL") ? atoi(getenv("LUTGEMM_POOL")) : 0;
-      int gmin = sh.RQ;
-      for (int fj = 0; fj < J; ++fj) gmin = std::min(gmin, p.gq[fj + 1] - p.gq[fj]);
-      p.pool_t = std::max(0, std::min(pool_env, gmin / 2));
     }
   }
   if (pa && (batched || p.fused_J <= 0)) return cudaErrorNotSupported;  // the fused epilogue only

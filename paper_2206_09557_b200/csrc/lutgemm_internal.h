@@ -55,8 +55,6 @@ struct KParams {
   int xdirect;       // GEMV: each thread loads its 8 x values for the LUT build straight from global memory
                      // (0: the slice is staged into shared memory by the bulk-copy engine first)
   int reducers;      // GEMV fused mode: the last R CTAs to arrive in a row-quad group reduce it
-  int pool_t;       // GEMV fused mode: the last pool_t row quads of every group form a per-slice pool
-                     // that the slice's CTAs claim quad by quad after their static share (0: off)
   // fused tensor-parallel epilogue over peer memory (NEXT-1, lutgemm_p2p.cu, gemv_kernel.cuh
   // p2p_epilogue): LL words (data | stamp << 32) into the ranks' windows.  p2p_mode 1 (rows
   // all-gather): rows (r, r+1) of the gathered output at window[par][pr] + 4 (yoff + r);
