@@ -51,3 +51,24 @@ def test_two_layer_stack_p2p_multi_process_same_gpu(nproc):
     assert d["finite"] and d["tp"] == nproc
     assert len(d["parity_rel_l2_sampled"]) == 12
     assert max(d["parity_rel_l2_sampled"].values()) <= 2e-3
+
+
+@pytest.mark.parametrize("nproc", [1, 2])
+def test_two_layer_stack_allgather_scheme(nproc):
+    """The contrast variant of SURVEY 8(e): every linear split by rows, y all-gathered through the fused
+    exchange (4 per layer); every linear's gathered output checked at this rank's rows against the oracle."""
+    script = [os.path.join(ROOT, "tools", "stack.py"), "--layers", "2", "--tokens", "3", "--check", "--tp-impl", "p2p",
+              "--tp-scheme", "allgather"]
+    if nproc == 1:
+        cmd = [sys.executable] + script
+    else:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+               "--master-addr", "127.0.0.1", "--master-port", str(29620 + nproc)] + script + ["--same-device"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, (out.stdout + out.stderr)[-3000:]
+    d = _stack_json(out)
+    assert d["finite"] and d["tp"] == nproc and d["tp_scheme"] == "allgather"
+    assert len(d["parity_rel_l2_sampled"]) == 16  # 8 shard checks + 8 gathered-output checks
+    assert max(d["parity_rel_l2_sampled"].values()) <= 2e-3
+    if nproc > 1:
+        assert d["allgathers_per_token"] == 8

@@ -16,6 +16,9 @@ and embeddings are omitted (the path is the linears): out-proj reads the first
 12288/P outputs of QKV.  Weights are seeded synthetic BCQ (device RNG), 73.4 GB
 at P=1.  One token = one CUDA graph of 384 LUT-GEMMs (+ 192 all-reduces).
 
+--tp-scheme allgather: the contrast variant of SURVEY 8(e) -- every linear split by rows and its y
+all-gathered (4 collectives per layer, 384 per token) instead of the Megatron pairing.
+
 --check: for layers 0 and L-1 each linear is also run on a seeded x and 64
 sampled rows are compared with the fp64 oracle (its inputs are the seeded
 canonical weights copied to the host before packing, never a CUDA output);
@@ -62,6 +65,10 @@ def main():
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--tp-impl", default="nccl", choices=["nccl", "p2p"])
     ap.add_argument("--same-device", action="store_true")
+    ap.add_argument("--tp-scheme", default="megatron", choices=["megatron", "allgather"],
+                    help="megatron: QKV / fc1 by rows, out / fc2 by columns + all-reduce (2 collectives per "
+                         "layer); allgather: every linear by rows + all-gather of y (4 per layer, the contrast "
+                         "variant of SURVEY 8(e))")
     ap.add_argument("--arena", action="store_true",
                     help="all packed weights in one device allocation (2 MB aligned views)")
     ap.add_argument("--graph-layers", type=int, default=0,
@@ -81,15 +88,17 @@ def main():
             comm = L.TPComm(rank, world, device=dev)
         else:
             dist.init_process_group("gloo")
+    ag = args.tp_scheme == "allgather"
+    linears = [(nm, m, n, "rows" if ag else sp) for nm, m, n, sp in LINEARS]
     if args.tp_impl == "p2p":
-        p2p = L.P2PGroup(rank, world, cols_m=H)
+        p2p = L.P2PGroup(rank, world, rows_out=4 * H if ag else 0, cols_m=0 if ag else H)
 
     t0 = time.time()
     arena, aoff = None, 0
     if args.arena:
         A2 = 2 << 20
         sizes = [(L.lutgemm_packed_bytes(m // world, n, Q, G, False) if s == "rows" else
-                  L.lutgemm_packed_bytes(m, n // world, Q, G, False)) for _, m, n, s in LINEARS]
+                  L.lutgemm_packed_bytes(m, n // world, Q, G, False)) for _, m, n, s in linears]
         arena = torch.empty(args.layers * sum((z + A2 - 1) // A2 * A2 for z in sizes) + A2, dtype=torch.uint8,
                             device=dev)
         aoff = (-arena.data_ptr()) % A2
@@ -98,7 +107,7 @@ def main():
     rng = np.random.default_rng(0)
     for layer in range(args.layers):
         lw = {}
-        for li, (name, m, n, split) in enumerate(LINEARS):
+        for li, (name, m, n, split) in enumerate(linears):
             ms, ns = (m // world, n) if split == "rows" else (m, n // world)
             seed = 1_000_003 * layer + 1009 * li + rank
             planes, alpha = gen_canonical(seed, ms, ns, dev)
@@ -124,16 +133,21 @@ def main():
     gx.manual_seed(2206)
     x0 = torch.randn(H, device=dev, generator=gx).to(torch.float16)  # seeded: x_sha is reproducible
     x = x0.clone()
-    qkv_o = torch.empty(3 * H // world, dtype=torch.float16, device=dev)
+    # (allgather: every output is gathered to its full length)
+    qkv_o = torch.empty(3 * H if ag else 3 * H // world, dtype=torch.float16, device=dev)
     out_o = torch.empty(H, dtype=torch.float16, device=dev)
-    fc1_o = torch.empty(4 * H // world, dtype=torch.float16, device=dev)
+    fc1_o = torch.empty(4 * H if ag else 4 * H // world, dtype=torch.float16, device=dev)
     ws_bytes = max(L.lutgemm_workspace_bytes(m // world if s == "rows" else m, n if s == "rows" else n // world, 1)
-                   for _, m, n, s in LINEARS)
+                   for _, m, n, s in linears)
     ws = L.make_workspace(ws_bytes, dev)
     tws = None
     if comm is not None:
-        tws = L.make_workspace(max(comm.workspace_bytes(L.TP_COLS_ALLREDUCE, H, H // world, 1),
-                                   comm.workspace_bytes(L.TP_COLS_ALLREDUCE, H, 4 * H // world, 1)), dev)
+        if ag:
+            tws = L.make_workspace(max(comm.workspace_bytes(L.TP_ROWS_ALLGATHER, m // world, n, 1)
+                                       for _, m, n, _s in linears), dev)
+        else:
+            tws = L.make_workspace(max(comm.workspace_bytes(L.TP_COLS_ALLREDUCE, H, H // world, 1),
+                                       comm.workspace_bytes(L.TP_COLS_ALLREDUCE, H, 4 * H // world, 1)), dev)
 
     def cols(w, xin, y):
         if p2p is not None:
@@ -143,10 +157,24 @@ def main():
         else:
             comm.linear(L.TP_COLS_ALLREDUCE, w, xin, y, tws)
 
+    def rows_ag(w, xin, y):  # row shard + all-gather of y (the allgather scheme)
+        if p2p is not None:
+            p2p.gemv_allgather(w, xin, ws, y)
+        elif comm is None:
+            L.lutgemm_gemv(w, xin, y, ws)
+        else:
+            comm.linear(L.TP_ROWS_ALLGATHER, w, xin, y, tws)
+
     def token(l0=0, l1=None):
         if l0 == 0:
             x.copy_(x0)  # every token starts from the same input (device-to-device copy)
         for lw in weights[l0:l1]:
+            if ag:
+                rows_ag(lw["qkv"], x, qkv_o)
+                rows_ag(lw["out"], qkv_o[:H], out_o)
+                rows_ag(lw["fc1"], out_o, fc1_o)
+                rows_ag(lw["fc2"], fc1_o, x)
+                continue
             L.lutgemm_gemv(lw["qkv"], x, qkv_o, ws)
             cols(lw["out"], qkv_o[:H // world], out_o)
             L.lutgemm_gemv(lw["fc1"], out_o, fc1_o, ws)
@@ -194,14 +222,22 @@ def main():
     for name in ("qkv", "out", "fc1", "fc2"):
         lw = weights[args.layers // 2]
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        xin, y = {"qkv": (x, qkv_o), "out": (qkv_o[:H // world], out_o), "fc1": (out_o, fc1_o),
+        xin, y = {"qkv": (x, qkv_o), "out": (qkv_o[:H] if ag else qkv_o[:H // world], out_o), "fc1": (out_o, fc1_o),
                   "fc2": (fc1_o, x)}[name]
+
+        def one():
+            if ag:
+                rows_ag(lw[name], xin, y)
+            elif name in ("qkv", "fc1"):
+                L.lutgemm_gemv(lw[name], xin, y, ws)
+            else:
+                cols(lw[name], xin, y)
         for _ in range(3):
-            (L.lutgemm_gemv(lw[name], xin, y, ws) if name in ("qkv", "fc1") else cols(lw[name], xin, y))
+            one()
         torch.cuda.synchronize()
         ev0.record()
         for _ in range(20):
-            (L.lutgemm_gemv(lw[name], xin, y, ws) if name in ("qkv", "fc1") else cols(lw[name], xin, y))
+            one()
         ev1.record()
         torch.cuda.synchronize()
         per[name] = round(ev0.elapsed_time(ev1) / 20 * 1e3, 2)
@@ -218,7 +254,14 @@ def main():
             got = y.float().cpu().numpy()[rows].astype(np.float64)
             ref = O.bcq_gemv(planes_rows, alpha_rows, None, xs[None], ns_, G)[0]
             parity[f"L{layer}.{name}"] = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
-            if name in ("out", "fc2") and (world > 1 or p2p is not None):
+            if ag and (world > 1 or p2p is not None):
+                # the gathered output: this rank's rows sit at rank * m_shard of the full vector
+                yfull = torch.empty(ms_ * world, dtype=torch.float16, device=dev)
+                rows_ag(weights[layer][name], torch.from_numpy(xs).to(dev), yfull)
+                torch.cuda.synchronize()
+                got = yfull.float().cpu().numpy()[rank * ms_ + rows].astype(np.float64)
+                parity[f"L{layer}.{name}.tp"] = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+            elif name in ("out", "fc2") and (world > 1 or p2p is not None):
                 # the TP output of the column split: sum over ranks of each shard's oracle partial
                 xf = np.random.default_rng(layer * 7 + len(name) + 1).standard_normal(ns_ * world).astype(np.float16)
                 xl = xf[rank * ns_:(rank + 1) * ns_]
@@ -233,7 +276,7 @@ def main():
                 parity[f"L{layer}.{name}.tp"] = float(np.linalg.norm(got - part) / np.linalg.norm(part))
 
     bytes_token = sum(((m // world) * n if s == "rows" else m * (n // world)) * (Q / 8 + 2 * Q / G)
-                      for _, m, n, s in LINEARS) * args.layers
+                      for _, m, n, s in linears) * args.layers
     if rank == 0:
         print(json.dumps({
             "config": "OPT-175B decoder linear stack (96 x QKV/out/fc1/fc2), q=3 g=128, b=1",
@@ -241,7 +284,9 @@ def main():
             "x_sha": x_sha,
             "ms_per_token": round(ms, 4),
             "GBps_per_gpu": round(bytes_token / (ms * 1e-3) / 1e9, 1),
-            "weight_bytes_per_gpu": int(bytes_token), "allreduces_per_token": 2 * args.layers if world > 1 else 0,
+            "weight_bytes_per_gpu": int(bytes_token), "tp_scheme": args.tp_scheme,
+            "allreduces_per_token": 2 * args.layers if world > 1 and not ag else 0,
+            "allgathers_per_token": 4 * args.layers if world > 1 and ag else 0,
             "per_linear_us_eager": per, "finite": finite, "build_s": round(build_s, 1),
             "hbm_alloc_gb": round(mem_gb, 1), "parity_rel_l2_sampled": parity,
             "paper_context_ms": "A100 FT e2e per token, 3-bit row-wise: 51.6 (1 GPU), 35.8 (2), 27.2 (4), 24.2 (8) (Table 4 P:L475-478)",
