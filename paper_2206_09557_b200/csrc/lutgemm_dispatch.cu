@@ -67,7 +67,21 @@ int batch_pad(int b) {
 size_t workspace_bytes(const Shape& sh, int b) {
   // b <= 4: sub-slice partials of the GEMV-structured kernel ([V S][b][m4], V = 2 or 4)
   const size_t slices = b == 2 ? 2 * (size_t)sh.S : (b <= 4 && b > 1 ? 4 * (size_t)sh.S : (size_t)sh.S);
-  return counters_bytes(sh) + (slices * (size_t)batch_pad(b) * (size_t)sh.m4 * 4u + 255) / 256 * 256;
+  const size_t own = counters_bytes(sh) + (slices * (size_t)batch_pad(b) * (size_t)sh.m4 * 4u + 255) / 256 * 256;
+  // b > 4 runs either the vector-slot kernel or (batch_split) chunks of <= 4 rows: room for both
+  return b > 4 ? std::max(own, workspace_bytes(sh, 4)) : own;
+}
+
+// b > 4 (and b = 3) as chunks of 4, 2 and 1 activation rows through the GEMV-structured kernels
+// instead of the vector-slot kernel (b > 4) or a padded V = 4 pass (b = 3): those run nearer their
+// shared-memory roof (fc1: b = 1 / 2 / 3 / 4 in 47 / 79 / 140 / 143 us against b = 5..8 in 318 us
+// in the vector-slot kernel, which pads to 8), and the re-read weights hide under the lookups.
+// A remainder of 3 runs as 2 + 1.  Not for chunk-group shapes (g % 32 != 0), which only the
+// vector-slot kernel serves.  LUTGEMM_BATCH_SPLIT=0 keeps the single launch (tests, sweeps).
+static bool batch_split(const Shape& sh, int b) {
+  static const int env = getenv("LUTGEMM_BATCH_SPLIT") ? atoi(getenv("LUTGEMM_BATCH_SPLIT")) : 1;
+  static const int vslot = getenv("LUTGEMM_SMALLB_BATCHED") ? atoi(getenv("LUTGEMM_SMALLB_BATCHED")) : 0;
+  return env && !vslot && (b > 4 || b == 3) && sh.gcls != kGrpChunk;
 }
 
 static unsigned long long* g_trace = nullptr;
@@ -105,6 +119,15 @@ static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint1
 
 cudaError_t run_product(const Shape& sh, const void* data, const uint16_t* x, int b, uint16_t* y, float* yf,
                         void* ws, cudaStream_t st) {
+  if (batch_split(sh, b)) {  // rows [c0, c0 + cb) of X and Y, one after the other on the stream
+    for (int c0 = 0, cb; c0 < b; c0 += cb) {
+      cb = b - c0 >= 4 ? 4 : (b - c0 == 3 ? 2 : b - c0);
+      const cudaError_t e = run_product_ex(sh, data, x + (size_t)c0 * sh.n, cb, y ? y + (size_t)c0 * sh.m : nullptr,
+                                           yf ? yf + (size_t)c0 * sh.m : nullptr, ws, st, nullptr);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
   return run_product_ex(sh, data, x, b, y, yf, ws, st, nullptr);
 }
 

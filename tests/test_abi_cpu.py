@@ -66,7 +66,9 @@ def test_abi_version_and_sizes():
     assert L.lutgemm_workspace_bytes(49152, 12288, 4) == 2304 + 4 * 12 * 4 * 49152 * 4
     assert L.lutgemm_workspace_bytes(5, 1056, 3) == 2304 + (4 * 2 * 4 * 8 * 4 + 255) // 256 * 256
     assert L.lutgemm_workspace_bytes(49152, 12288, 2) == 2304 + 2 * 12 * 2 * 49152 * 4
-    assert L.lutgemm_workspace_bytes(49152, 12288, 8) == 2304 + 12 * 8 * 49152 * 4
+    # b > 4: room for the vector-slot kernel ([S][b_pad][m4]) and for chunks of <= 4 rows (the b = 4 partials)
+    assert L.lutgemm_workspace_bytes(49152, 12288, 8) == 2304 + 4 * 12 * 4 * 49152 * 4
+    assert L.lutgemm_workspace_bytes(49152, 12288, 32) == 2304 + 12 * 32 * 49152 * 4
 
 
 @pytest.mark.parametrize("m,n,q,g", [(0, 64, 3, 32), (8, 64, 0, 32), (8, 64, 9, 32), (8, 96, 3, 64),
