@@ -14,6 +14,6 @@ timeout 900 python tools/sweep.py --steps 300 > gpurun_out/sweep_$TAG.jsonl 2> g
 timeout 600 python tools/stack.py > gpurun_out/stack_$TAG.json 2> gpurun_out/stack_$TAG.err; tail -1 gpurun_out/stack_$TAG.json
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 20 --warmup 3 --no-cpu --no-check > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:lut_gemv -s 10 -c 1 -o gpurun_out/prof_$TAG python bench.py --steps 20 --warmup 5 --no-cpu --no-check > gpurun_out/ncu_$TAG.log 2>&1; tail -1 gpurun_out/ncu_$TAG.log
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:lut_gemm_batched -s 1 -c 1 -o gpurun_out/prof_b8_$TAG python tools/run_once.py 49152 12288 3 128 8 > gpurun_out/ncu_b8_$TAG.log 2>&1; tail -1 gpurun_out/ncu_b8_$TAG.log
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:lut_gemvv -s 1 -c 1 -o gpurun_out/prof_b8_$TAG python tools/run_once.py 49152 12288 3 128 8 > gpurun_out/ncu_b8_$TAG.log 2>&1; tail -1 gpurun_out/ncu_b8_$TAG.log
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:lut_gemvv -s 1 -c 1 -o gpurun_out/prof_b2_$TAG python tools/run_once.py 49152 12288 3 128 2 > gpurun_out/ncu_b2_$TAG.log 2>&1; tail -1 gpurun_out/ncu_b2_$TAG.log
 timeout 600 python tools/trace_spread.py > gpurun_out/trace_$TAG.jsonl 2>&1; tail -4 gpurun_out/trace_$TAG.jsonl | cut -c1-300
