@@ -16,6 +16,9 @@ and embeddings are omitted (the path is the linears): out-proj reads the first
 12288/P outputs of QKV.  Weights are seeded synthetic BCQ (device RNG), 73.4 GB
 at P=1.  One token = one CUDA graph of 384 LUT-GEMMs (+ 192 all-reduces).
 
+--shard-tp N (world 1): rank 0's shards of TP N run without any exchange -- the per-GPU compute of
+TP-N per-token latency, the part one GPU can measure (the exchange adds 2 collectives per layer).
+
 --tp-scheme allgather: the contrast variant of SURVEY 8(e) -- every linear split by rows and its y
 all-gathered (4 collectives per layer, 384 per token) instead of the Megatron pairing.
 
@@ -65,6 +68,8 @@ def main():
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--tp-impl", default="nccl", choices=["nccl", "p2p"])
     ap.add_argument("--same-device", action="store_true")
+    ap.add_argument("--shard-tp", type=int, default=0,
+                    help="world 1 only: run rank 0's shards of TP N (1/2/4/8) without the exchange")
     ap.add_argument("--tp-scheme", default="megatron", choices=["megatron", "allgather"],
                     help="megatron: QKV / fc1 by rows, out / fc2 by columns + all-reduce (2 collectives per "
                          "layer); allgather: every linear by rows + all-gather of y (4 per layer, the contrast "
@@ -77,6 +82,13 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    # shard size: the TP degree (or, at world 1, --shard-tp N: rank 0's shards of TP N without the
+    # exchange -- the per-GPU compute part of TP-N latency, measurable on one GPU)
+    sw = world
+    if args.shard_tp:
+        if world > 1:
+            raise SystemExit("--shard-tp is a world-1 option")
+        sw = args.shard_tp
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dev = torch.device("cuda", 0 if args.same_device else local)
     torch.cuda.set_device(dev)
@@ -97,8 +109,8 @@ def main():
     arena, aoff = None, 0
     if args.arena:
         A2 = 2 << 20
-        sizes = [(L.lutgemm_packed_bytes(m // world, n, Q, G, False) if s == "rows" else
-                  L.lutgemm_packed_bytes(m, n // world, Q, G, False)) for _, m, n, s in linears]
+        sizes = [(L.lutgemm_packed_bytes(m // sw, n, Q, G, False) if s == "rows" else
+                  L.lutgemm_packed_bytes(m, n // sw, Q, G, False)) for _, m, n, s in linears]
         arena = torch.empty(args.layers * sum((z + A2 - 1) // A2 * A2 for z in sizes) + A2, dtype=torch.uint8,
                             device=dev)
         aoff = (-arena.data_ptr()) % A2
@@ -108,7 +120,7 @@ def main():
     for layer in range(args.layers):
         lw = {}
         for li, (name, m, n, split) in enumerate(linears):
-            ms, ns = (m // world, n) if split == "rows" else (m, n // world)
+            ms, ns = (m // sw, n) if split == "rows" else (m, n // sw)
             seed = 1_000_003 * layer + 1009 * li + rank
             planes, alpha = gen_canonical(seed, ms, ns, dev)
             if args.check and layer in (0, args.layers - 1):
@@ -134,20 +146,20 @@ def main():
     x0 = torch.randn(H, device=dev, generator=gx).to(torch.float16)  # seeded: x_sha is reproducible
     x = x0.clone()
     # (allgather: every output is gathered to its full length)
-    qkv_o = torch.empty(3 * H if ag else 3 * H // world, dtype=torch.float16, device=dev)
+    qkv_o = torch.empty(3 * H if ag else 3 * H // sw, dtype=torch.float16, device=dev)
     out_o = torch.empty(H, dtype=torch.float16, device=dev)
-    fc1_o = torch.empty(4 * H if ag else 4 * H // world, dtype=torch.float16, device=dev)
-    ws_bytes = max(L.lutgemm_workspace_bytes(m // world if s == "rows" else m, n if s == "rows" else n // world, 1)
+    fc1_o = torch.empty(4 * H if ag else 4 * H // sw, dtype=torch.float16, device=dev)
+    ws_bytes = max(L.lutgemm_workspace_bytes(m // sw if s == "rows" else m, n if s == "rows" else n // sw, 1)
                    for _, m, n, s in linears)
     ws = L.make_workspace(ws_bytes, dev)
     tws = None
     if comm is not None:
         if ag:
-            tws = L.make_workspace(max(comm.workspace_bytes(L.TP_ROWS_ALLGATHER, m // world, n, 1)
+            tws = L.make_workspace(max(comm.workspace_bytes(L.TP_ROWS_ALLGATHER, m // sw, n, 1)
                                        for _, m, n, _s in linears), dev)
         else:
-            tws = L.make_workspace(max(comm.workspace_bytes(L.TP_COLS_ALLREDUCE, H, H // world, 1),
-                                       comm.workspace_bytes(L.TP_COLS_ALLREDUCE, H, 4 * H // world, 1)), dev)
+            tws = L.make_workspace(max(comm.workspace_bytes(L.TP_COLS_ALLREDUCE, H, H // sw, 1),
+                                       comm.workspace_bytes(L.TP_COLS_ALLREDUCE, H, 4 * H // sw, 1)), dev)
 
     def cols(w, xin, y):
         if p2p is not None:
@@ -176,7 +188,7 @@ def main():
                 rows_ag(lw["fc2"], fc1_o, x)
                 continue
             L.lutgemm_gemv(lw["qkv"], x, qkv_o, ws)
-            cols(lw["out"], qkv_o[:H // world], out_o)
+            cols(lw["out"], qkv_o[:H // sw], out_o)
             L.lutgemm_gemv(lw["fc1"], out_o, fc1_o, ws)
             cols(lw["fc2"], fc1_o, x)
 
@@ -222,7 +234,7 @@ def main():
     for name in ("qkv", "out", "fc1", "fc2"):
         lw = weights[args.layers // 2]
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        xin, y = {"qkv": (x, qkv_o), "out": (qkv_o[:H] if ag else qkv_o[:H // world], out_o), "fc1": (out_o, fc1_o),
+        xin, y = {"qkv": (x, qkv_o), "out": (qkv_o[:H] if ag else qkv_o[:H // sw], out_o), "fc1": (out_o, fc1_o),
                   "fc2": (fc1_o, x)}[name]
 
         def one():
@@ -275,12 +287,13 @@ def main():
                 got = y.float().cpu().numpy()[rows].astype(np.float64)
                 parity[f"L{layer}.{name}.tp"] = float(np.linalg.norm(got - part) / np.linalg.norm(part))
 
-    bytes_token = sum(((m // world) * n if s == "rows" else m * (n // world)) * (Q / 8 + 2 * Q / G)
+    bytes_token = sum(((m // sw) * n if s == "rows" else m * (n // sw)) * (Q / 8 + 2 * Q / G)
                       for _, m, n, s in linears) * args.layers
     if rank == 0:
         print(json.dumps({
             "config": "OPT-175B decoder linear stack (96 x QKV/out/fc1/fc2), q=3 g=128, b=1",
-            "layers": args.layers, "graph_layers": gl, "arena": args.arena, "tp": world, "tp_impl": args.tp_impl if world > 1 or p2p else None,
+            "layers": args.layers, "graph_layers": gl, "arena": args.arena, "tp": world,
+            "shard_tp": sw if args.shard_tp else None, "tp_impl": args.tp_impl if world > 1 or p2p else None,
             "x_sha": x_sha,
             "ms_per_token": round(ms, 4),
             "GBps_per_gpu": round(bytes_token / (ms * 1e-3) / 1e9, 1),
