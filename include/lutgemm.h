@@ -284,7 +284,9 @@ int lutgemm_tp_nranks(const lutgemm_tp* tp);
  *    LUTGEMM_ERR_INVALID_ARG.
  * The round number lives on the device, so calls are CUDA-graph capturable; each rank owns two
  * windows (double buffer by round parity).  Every rank must make the same sequence of calls on
- * a group.  y is complete when the call's kernel completes on the stream. */
+ * a group.  y is complete when the call's kernel completes on the stream.  A reader that sees no
+ * word from a peer for 30 s (env LUTGEMM_P2P_TIMEOUT_MS) traps: the launch fails (a sticky CUDA
+ * error) instead of hanging. */
 typedef struct lutgemm_p2p lutgemm_p2p;
 
 /* Bytes of one exchange window for `mode` (LUTGEMM_TP_ROWS_ALLGATHER: m = rows of the gathered

@@ -69,12 +69,18 @@ __device__ __forceinline__ void st_ll(uint8_t* p, uint32_t d, uint32_t stamp) {
   const unsigned long long w = ((unsigned long long)stamp << 32) | d;
   asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
 }
-__device__ __forceinline__ uint32_t ld_ll(const uint8_t* p, uint32_t stamp) {
+// a peer that never writes (crashed, or a call sequence that differs between ranks) must not hang
+// the GPU: after timeout_ns without the round's word the kernel traps (the launch fails loudly)
+__device__ __forceinline__ uint32_t ld_ll(const uint8_t* p, uint32_t stamp, unsigned long long timeout_ns) {
   unsigned long long w;
   asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
-  while ((uint32_t)(w >> 32) != stamp) {
-    __nanosleep(16);
-    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+  if ((uint32_t)(w >> 32) != stamp) {
+    const unsigned long long t0 = globaltimer_ns();
+    do {
+      __nanosleep(16);
+      asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+      if (globaltimer_ns() - t0 > timeout_ns) __trap();
+    } while ((uint32_t)(w >> 32) != stamp);
   }
   return (uint32_t)w;
 }
@@ -136,7 +142,7 @@ __device__ __forceinline__ void p2p_epilogue(const KParams& p, unsigned long lon
       if (r < r1 && !(lane & 1))
         for (int k = 0; k < P - 1; ++k) {
           const int pr = k + (k >= self ? 1 : 0), rr = pr * ms + r;
-          const uint32_t w = ld_ll(mine + 4 * (size_t)rr, stamp);
+          const uint32_t w = ld_ll(mine + 4 * (size_t)rr, stamp, p.p2p_timeout_ns);
           p.y[rr] = __ushort_as_half((unsigned short)(w & 0xFFFFu));
           p.y[rr + 1] = __ushort_as_half((unsigned short)(w >> 16));
         }
@@ -157,7 +163,7 @@ __device__ __forceinline__ void p2p_epilogue(const KParams& p, unsigned long lon
       float sum = 0.f;
       if (own)
         for (int pr = 0; pr < P; ++pr)
-          sum += pr == self ? v : __uint_as_float(ld_ll(mine + 8 * ((size_t)pr * mb + (r - o * mb)), stamp));
+          sum += pr == self ? v : __uint_as_float(ld_ll(mine + 8 * ((size_t)pr * mb + (r - o * mb)), stamp, p.p2p_timeout_ns));
       const __half h = __float2half_rn(sum);
       if (own) p.y[r] = h;
       if (P > 1) {
@@ -172,7 +178,7 @@ __device__ __forceinline__ void p2p_epilogue(const KParams& p, unsigned long lon
       for (int base = r0 + (tid & ~31); base < r1; base += kThreads) {
         const int r = base + lane;
         if (r < r1 && !(lane & 1) && r / mb != self) {
-          const uint32_t w = ld_ll(mine + p.p2p_yarea + 4 * (size_t)r, stamp);
+          const uint32_t w = ld_ll(mine + p.p2p_yarea + 4 * (size_t)r, stamp, p.p2p_timeout_ns);
           p.y[r] = __ushort_as_half((unsigned short)(w & 0xFFFFu));
           if (r + 1 < m) p.y[r + 1] = __ushort_as_half((unsigned short)(w >> 16));
         }

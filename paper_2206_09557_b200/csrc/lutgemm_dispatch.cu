@@ -148,6 +148,10 @@ static cudaError_t run_product_ex(const Shape& sh, const void* data, const uint1
   p.p2p_mb = pa ? pa->mb : 0;
   p.p2p_yarea = pa ? pa->yarea : 0;
   p.p2p_round = pa ? pa->round : nullptr;
+  {
+    static const long long tmo = getenv("LUTGEMM_P2P_TIMEOUT_MS") ? atoll(getenv("LUTGEMM_P2P_TIMEOUT_MS")) : 30000;
+    p.p2p_timeout_ns = (unsigned long long)std::max(1LL, tmo) * 1000000ull;
+  }
   for (int i = 0; i < 8; ++i) {
     const bool on = pa && i < pa->npeers;
     p.p2p_win[0][i] = on ? pa->win[0][i] : nullptr;

@@ -64,6 +64,7 @@ struct KParams {
   uint8_t* p2p_win[2][8];
   const unsigned long long* p2p_round;
   int p2p_mode;      // 0: plain output
+  unsigned long long p2p_timeout_ns;  // an LL wait longer than this traps (LUTGEMM_P2P_TIMEOUT_MS, default 30 s)
   int npeers;
   int yoff;
   int p2p_self;

@@ -130,3 +130,19 @@ def test_p2p_world1_graph_capture():
                             "--mode", mode], capture_output=True, text=True, timeout=600, cwd=ROOT)
         out = r.stdout + r.stderr
         assert r.returncode == 0 and out.count(": PASS") == 5, out[-3000:]
+
+
+def test_p2p_dead_peer_traps_instead_of_hanging():
+    """Failure detection: a peer that never makes its call makes the waiting rank's fused
+    exchange trap after LUTGEMM_P2P_TIMEOUT_MS (here 2 s) -- a loud launch failure, not a GPU hang."""
+    import time
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, LUTGEMM_P2P_TIMEOUT_MS="2000")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", "--master-port", "29641", os.path.join(root, "tools", "p2p_timeout.py")]
+    t0 = time.time()
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=root, env=env)
+    text = out.stdout + out.stderr
+    assert out.returncode == 0, text[-3000:]
+    assert "p2p timeout: trapped" in text, text[-3000:]
+    assert time.time() - t0 < 240
