@@ -90,11 +90,12 @@ def main(tag, rnd="01"):
             "issue_active_pct": round(num(g, "smsp__issue_active.avg.pct_of_peak_sustained_active"), 2),
             "lsu_pipe_pct": round(num(g, "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"), 2),
         },
-        "lut_gemm_batched_kernel": {
-            "kernel": f"{bname} (fc1, b=8)",
-            "source": f"ncu --set full --clock-control none -k regex:lut_gemm_batched -s 1 -c 1, tag {tag}",
+        "batched_b8_kernel": {
+            # b = 8 runs as two b = 4 chunks (batch split): the capture is one chunk's lut_gemvv_kernel
+            "kernel": f"{bname} (fc1, b=8: one of its two b=4 chunks)",
+            "source": f"ncu --set full --clock-control none -k regex:lut_gemvv -s 1 -c 1, tag {tag}",
             "dram_bytes_per_launch": int(num(b8, "dram__bytes_read.sum") + num(b8, "dram__bytes_write.sum")),
-            "algorithmic_bytes": algorithmic_bytes(49152, 12288, 3, 128, 8),
+            "algorithmic_bytes": algorithmic_bytes(49152, 12288, 3, 128, 4),
             "ncu_duration_us": round(num(b8, "gpu__time_duration.sum"), 3),
             "shared_wavefronts": int(num(b8, "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum")),
             "shared_ld_bank_conflicts": int(num(b8, "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum")),
