@@ -200,7 +200,8 @@ def main(tag, rnd="01"):
     open(os.path.join(PROF, f"r{rnd}_sweep.md"), "w").write("\n".join(t) + "\n")
     # sanitizers (tools/sanitize.sh), if that run is present
     san = {t: os.path.join(OUT, f"sanitize_{t}.txt") for t in ("memcheck", "racecheck", "synccheck", "initcheck")}
-    if all(os.path.exists(v) for v in san.values()):
+    closed = any("closed on this pool" in open(v).read() for v in san.values() if os.path.exists(v))
+    if all(os.path.exists(v) for v in san.values()) and not closed:
         sl = [f"# Round {int(rnd)} -- compute-sanitizer over every kernel path (SURVEY 4, tier T4)", "",
               "Command: `bash tools/sanitize.sh` (runs `tools/sanitize_case.py` under each tool: GEMV fused and "
               "non-fused with one and many reducers, n and m tails, batched V=2 and V=4, q up to 6, fp32 output, "
