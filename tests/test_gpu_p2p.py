@@ -123,6 +123,18 @@ def test_p2p_multi_process_same_gpu(nproc, mode, graph):
     assert out.count(": PASS") == 4 * nproc and ": FAIL" not in out, out[-3000:]
 
 
+@pytest.mark.parametrize("mode,nproc,rows,cols", [("rows", 4, 1184, 4096), ("cols", 4, 1000, 8192),
+                                                   ("cols", 2, 1001, 4096)])
+def test_p2p_multi_process_uneven_shapes(mode, nproc, rows, cols):
+    """Shards whose rows do not fill the 8-row units and owner blocks evenly: rows 1184 / 4 = 296 per
+    rank; cols m = 1000 over 4 owners (blocks 256, 256, 256, 232) and an odd m = 1001 over 2 owners
+    (the last LL word carries one real row); column shards of 2048 (2 LUT slices: the fused mode needs
+    at least one 8-row unit per CTA).  Back-to-back rounds, every rank against the oracle."""
+    port = 29570 + nproc + (10 if mode == "cols" else 0) + (rows % 7)
+    out = _run_check(nproc, port, "--rounds", "3", "--mode", mode, "--rows", str(rows), "--cols", str(cols))
+    assert out.count(": PASS") == 3 * nproc and ": FAIL" not in out, out[-3000:]
+
+
 def test_p2p_world1_graph_capture():
     """World 1, both modes: a CUDA graph of rounds replays correctly (device-side round counter)."""
     for mode in ("rows", "cols"):
