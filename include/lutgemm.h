@@ -293,7 +293,7 @@ typedef struct lutgemm_p2p lutgemm_p2p;
  * output, P * m_shard; LUTGEMM_TP_COLS_ALLREDUCE: m = rows of the layer); 0 on bad arguments.
  * A group serves every call whose need is <= its window size. */
 size_t lutgemm_p2p_window_bytes(int nranks, int mode, int m);
-/* Allocate this rank's two windows (win_bytes each, device) and signal block and write a 256-byte
+/* Allocate this rank's two windows (win_bytes each, device) and its (local) round word and write a 256-byte
  * exchange record (CUDA IPC handles, rank, sizes) that the caller gathers from all ranks, in rank
  * order, by any transport.  1 <= nranks <= 8.  Collective in the sense that every rank creates
  * one group with the same win_bytes. */

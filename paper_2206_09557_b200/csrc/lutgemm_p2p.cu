@@ -52,7 +52,6 @@ struct lutgemm_p2p {
   uint8_t* win[2];                     // local windows
   unsigned long long* sig;             // local signal block
   uint8_t* peer_win[2][8];             // every rank's windows in this process's address space (self: local)
-  unsigned long long* peer_sig[8];
   bool connected;
 };
 
@@ -60,7 +59,7 @@ namespace {
 
 using namespace lg;
 
-constexpr int kRec = 256;  // record: 3 IPC handles (64 B each), rank, window bytes
+constexpr int kRec = 256;  // record: 2 IPC handles (the windows, 64 B each), 64 B unused, rank, window bytes
 
 lutgemm_status cuda_fail(cudaError_t e, const char* what) {
   char buf[384];
@@ -151,15 +150,14 @@ lutgemm_status lutgemm_p2p_create(int rank, int nranks, size_t win_bytes, lutgem
   if (e == cudaSuccess) e = cudaMemset(g->win[0], 0, g->win_bytes);
   if (e == cudaSuccess) e = cudaMemset(g->win[1], 0, g->win_bytes);
   memset(record, 0, kRec);
-  cudaIpcMemHandle_t h[3];
+  cudaIpcMemHandle_t h[2];  // the windows (the signal block holds only the local round: not shared)
   if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h[0], g->win[0]);
   if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h[1], g->win[1]);
-  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h[2], g->sig);
   if (e != cudaSuccess) {
     lutgemm_p2p_destroy(g);
     return cuda_fail(e, "p2p windows / IPC handles");
   }
-  memcpy(record, h, 3 * 64);
+  memcpy(record, h, 2 * 64);
   memcpy(record + 192, &rank, sizeof(int));
   const unsigned long long wb = g->win_bytes;
   memcpy(record + 200, &wb, sizeof(wb));
@@ -182,13 +180,12 @@ lutgemm_status lutgemm_p2p_connect(lutgemm_p2p* g, const uint8_t* records) {
     if (pr == g->rank) {
       g->peer_win[0][pr] = g->win[0];
       g->peer_win[1][pr] = g->win[1];
-      g->peer_sig[pr] = g->sig;
       continue;
     }
-    cudaIpcMemHandle_t h[3];
-    memcpy(h, records + (size_t)pr * kRec, 3 * 64);
-    void* p[3] = {nullptr, nullptr, nullptr};
-    for (int i = 0; i < 3; ++i) {
+    cudaIpcMemHandle_t h[2];
+    memcpy(h, records + (size_t)pr * kRec, 2 * 64);
+    void* p[2] = {nullptr, nullptr};
+    for (int i = 0; i < 2; ++i) {
       cudaError_t e = cudaIpcOpenMemHandle(&p[i], h[i], cudaIpcMemLazyEnablePeerAccess);
       if (e != cudaSuccess) {
         // close what this call opened (this peer's and every earlier peer's mappings)
@@ -197,16 +194,13 @@ lutgemm_status lutgemm_p2p_connect(lutgemm_p2p* g, const uint8_t* records) {
           if (q == g->rank) continue;
           cudaIpcCloseMemHandle(g->peer_win[0][q]);
           cudaIpcCloseMemHandle(g->peer_win[1][q]);
-          cudaIpcCloseMemHandle(g->peer_sig[q]);
           g->peer_win[0][q] = g->peer_win[1][q] = nullptr;
-          g->peer_sig[q] = nullptr;
         }
         return cuda_fail(e, "cudaIpcOpenMemHandle");
       }
     }
     g->peer_win[0][pr] = static_cast<uint8_t*>(p[0]);
     g->peer_win[1][pr] = static_cast<uint8_t*>(p[1]);
-    g->peer_sig[pr] = static_cast<unsigned long long*>(p[2]);
   }
   g->connected = true;
   return LUTGEMM_OK;
@@ -232,7 +226,6 @@ lutgemm_status lutgemm_p2p_destroy(lutgemm_p2p* g) {
     if (pr == g->rank) continue;
     if (g->peer_win[0][pr]) cudaIpcCloseMemHandle(g->peer_win[0][pr]);
     if (g->peer_win[1][pr]) cudaIpcCloseMemHandle(g->peer_win[1][pr]);
-    if (g->peer_sig[pr]) cudaIpcCloseMemHandle(g->peer_sig[pr]);
   }
   if (g->win[0]) cudaFree(g->win[0]);
   if (g->win[1]) cudaFree(g->win[1]);
