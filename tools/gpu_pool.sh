@@ -1,4 +1,5 @@
 #!/bin/bash
+# HISTORICAL: the LUTGEMM_POOL knob was removed after this experiment (profiles/r02_tail_pool_dropped.md)
 # A/B of the GEMV tail pool (LUTGEMM_POOL = quads per group moved to the per-slice pool)
 mkdir -p gpurun_out
 CASES=49152:12288:3:128,12288:49152:3:128,12288:12288:3:128,12288:12288:1:128,8192:8192:4:128:1:1,22016:8192:4:128:1:1,8192:22016:4:128:1:1

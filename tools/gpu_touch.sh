@@ -1,4 +1,5 @@
 #!/bin/bash
+# HISTORICAL: the LUTGEMM_TOUCH knob was removed after this experiment (DESIGN "Measured and dropped")
 # A/B of LUTGEMM_TOUCH (translation warm-up before the PDL wait): chain over k distinct copies, 96-layer stack
 set -u
 mkdir -p gpurun_out
